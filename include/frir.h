@@ -1,0 +1,185 @@
+/*
+ * frir.h -- C ABI of the B200-native FRAM-RIR generator (libfrir.so).
+ *
+ * The reference (arxiv 2304.08052, /root/reference/pkg) has no native FFI: its
+ * drop-in boundary is the pure-Python call
+ *     framrir.simulate_rir(params, scene, include_early=True)   core.py:268-316
+ * and the dataloader veneer
+ *     framrir_binding.py_simulate_rir(config, include_early)    binding/.../__init__.py:66-94
+ * Both are mirrored in Python by paper_2304_08052_b200 (same names, arguments,
+ * defaults and ValueError texts) on top of the entry points declared here.
+ * Each entry point below names the reference function(s) whose arithmetic it
+ * replaces.  Plain C types only: no torch, no C++ across the boundary.
+ *
+ * Conventions
+ *   - Every function returns FRIR_OK (0) or a negative status; the message of
+ *     the last failure on the calling thread is in frir_last_error().
+ *   - Device pointers are allocated by the caller (the library never allocates
+ *     on the hot path); `stream` is a cudaStream_t passed as void*.
+ *   - frir_simulate is asynchronous on `stream` and re-entrant across streams
+ *     (the plan is read-only after creation).
+ */
+#ifndef FRIR_H_
+#define FRIR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FRIR_ABI_VERSION 1
+
+enum {
+  FRIR_OK = 0,
+  FRIR_EINVAL = -1, /* invalid argument (reference ValueError) */
+  FRIR_ECUDA = -2,  /* CUDA runtime / launch failure */
+  FRIR_ERANGE = -3, /* size outside what the kernels support */
+  FRIR_ENOMEM = -4  /* workspace too small */
+};
+
+/* Table ids for frir_design_table (host-only test hooks). */
+enum {
+  FRIR_TAB_H1 = 0,        /* stage-1 Kaiser taps, resample.py:74-78 (firwin, unscaled) */
+  FRIR_TAB_H2 = 1,        /* stage-2 Kaiser taps */
+  FRIR_TAB_SOS = 2,       /* 80 Hz Butterworth HP section [b0 b1 b2 1 a1 a2], resample.py:109 */
+  FRIR_TAB_COMP_D = 3,    /* composite decimation table, t in [t0, t0 + r_h*sup) */
+  FRIR_TAB_COMP_W = 4,    /* composite low-pass-branch table, same t range */
+  FRIR_TAB_KAPPA = 5,     /* tail-correction state gains, [half2][2] */
+  FRIR_TAB_U = 6,         /* tail-correction input response (h2 * HP impulse), [half2] */
+  FRIR_TAB_ZPHASE = 7,    /* per-phase modal tap sums, [down][2] (re, im) */
+  FRIR_TAB_PPOW = 8,      /* p^m, m < horizon, [horizon][2] (re, im) */
+  FRIR_TAB_LPCOEF = 9     /* [c1, c2, v0 (4 doubles: re0 im0 re1 im1)] */
+};
+
+typedef struct frir_plan frir_plan;
+
+/* Per-sample-rate constants (resample.py:59-71 rate_factors, :74-78, :107-113). */
+typedef struct {
+  int32_t sample_rate;
+  int32_t r_h, r_l;          /* rate factors: r_h = 10^6 // fs, r_l = isqrt(r_h) */
+  int32_t up, down;          /* stage-1 ratio reduced by gcd (scipy resample_poly) */
+  int32_t half1, len1;       /* stage-1 taps: 2*half1 + 1 */
+  int32_t half2, len2;       /* stage-2 taps */
+  int32_t t0, sup;           /* composite support: t in [t0, t0 + r_h*sup) */
+  int32_t nb;                /* look-back windows for the 32-sample gather */
+  int32_t horizon;           /* mid-rate samples of HP memory kept by the tail fix */
+  int32_t lt_max;            /* max stage-1 taps past n1 */
+  int32_t pad_;
+  double sos[6];             /* [b0 b1 b2 1 a1 a2] */
+  double c1, c2;             /* output-rate LP recursion */
+} frir_plan_desc;
+
+/*
+ * One RIR job = one (room, source).  Inputs mirror SimParams (params.py:38-47)
+ * and Scene (params.py:77-80).  Layout/derived fields are filled by
+ * frir_jobs_prepare() on the host.  Keep in sync with
+ * paper_2304_08052_b200/_abi.py (numpy structured dtype).
+ */
+typedef struct {
+  /* ---- inputs ---- */
+  double room[3];            /* room_dims (m) */
+  double center[3];          /* array reference point in the mic frame (params.py:149-153) */
+  double d0, az, el;         /* source (distance, azimuth, elevation) rel. to center */
+  double t60;                /* SimParams.t60 */
+  double c0;                 /* SimParams.sound_speed */
+  double alpha, beta;        /* distance-ratio support */
+  double perturb_lo, perturb_hi;
+  double tau;
+  uint64_t seed;             /* SimParams.seed (0 <= seed < 2^64) */
+  int32_t source_index;      /* k: Philox stream (seed, k, stage), core.py:86-91 */
+  int32_t n_images;          /* I (SimParams.num_images), per job */
+  int32_t mic_off;           /* first mic row in frir_batch.mics */
+  int32_t n_mics;            /* M */
+  /* ---- layout (frir_jobs_prepare) ---- */
+  int64_t img_off;           /* first image row (row 0 = direct path) */
+  int64_t item_off;          /* first (image, mic) item */
+  int64_t out_off;           /* first output sample (floats) */
+  int32_t chan_off;          /* first channel */
+  int32_t out_stride;        /* floats between channel rows */
+  int32_t L;                 /* high-rate train length ceil(t60 * r_h * fs) */
+  int32_t n1, n2;            /* mid / output lengths */
+  int32_t pad_;
+  /* ---- derived (frir_jobs_prepare) ---- */
+  double r;                  /* reflection coefficient, core.py:113-128 */
+  double rr_max;             /* max_reflections, core.py:186-192 (0 when I == 0) */
+  double alpha3, b3a3;       /* alpha**3 and beta**3 - alpha**3 (core.py:100) */
+  uint64_t key[4];          /* Philox keys of streams (seed, k, 0) and (seed, k, 1) */
+} frir_job;
+
+typedef struct {
+  const frir_job* jobs;      /* device, n_jobs entries */
+  int32_t n_jobs;
+  int32_t total_channels;    /* sum of n_mics */
+  const int32_t* chan_job;   /* device, job index of every channel */
+  const int32_t* chan_order; /* device, processing order of channels (longest first) or NULL */
+  const double* mics;        /* device, mic rows (x, y, z) */
+  /* Oracle mode: the reference's own draws (ImageSet fields, core.py:43-62),
+     indexed img_off + i for i in [1, I]; all NULL in native mode. */
+  const double* draw_dist;   /* ImageSet.distances   */
+  const double* draw_az;     /* ImageSet.azimuths    */
+  const double* draw_el;     /* ImageSet.elevations  */
+  const double* draw_refl;   /* ImageSet.reflections */
+  int64_t total_images;      /* sum (I + 1) */
+  int64_t total_items;       /* sum M (I + 1) */
+  int64_t total_out;         /* floats per output buffer */
+  int32_t max_rows;          /* max (I + 1) */
+  int32_t max_windows;       /* max ceil((n2 + 10) / 32) */
+} frir_batch;
+
+/* ---- plans ---------------------------------------------------------------- */
+
+/* Host filter design (firwin/kaiser/butter restated, composite tables) and upload
+   to the current CUDA device.  Replaces resample.py:74-78,107-113 setup. */
+int frir_plan_create(int32_t sample_rate, frir_plan** out);
+int frir_plan_describe(const frir_plan* plan, frir_plan_desc* out);
+int frir_plan_destroy(frir_plan* plan);
+
+/* Host-only (no GPU): design tables for tests.  Writes up to `cap` doubles. */
+int frir_design_describe(int32_t sample_rate, frir_plan_desc* out);
+int frir_design_table(int32_t sample_rate, int32_t which, double* out, int64_t cap,
+                      int64_t* n_out);
+
+/* Host-only (no GPU): uniform doubles of numpy's
+   Generator(Philox(SeedSequence((seed, k, stage)))).random(), words
+   [first, first + n).  Restates core.py:86-91 + numpy 2.x Philox4x64-10. */
+int frir_philox_doubles(uint64_t seed, uint64_t source_index, uint64_t stage,
+                        uint64_t first_word, int64_t n, double* out);
+
+/* ---- batches -------------------------------------------------------------- */
+
+/* Host (no GPU): validate jobs (reference ValueError rules, core.py:113-128,140-148,186-192,
+   209-210) and fill layout + derived fields.  `padded` != 0 lays the outputs out
+   as [job][mic][max_n2]; otherwise packed.  Fills the totals of `batch` (pointers
+   untouched).  chan_job / chan_order (nullable, sum(n_mics) entries each)
+   receive the job of every channel and a longest-first processing order. */
+int frir_jobs_prepare(int32_t sample_rate, frir_job* jobs_host, int32_t n_jobs,
+                      int32_t padded, frir_batch* batch, int32_t* chan_job,
+                      int32_t* chan_order);
+
+/* Bytes of device workspace frir_simulate needs for `batch`. */
+size_t frir_workspace_size(const frir_plan* plan, const frir_batch* batch);
+
+/* Render every job of the batch: full (and, if out_early != NULL, early) RIRs.
+   Replaces core.py:131-265 (sampling, delays, train, early window) and
+   resample.py:81-136 (both decimation stages and the HP).  direct_index gets
+   RirFilter.direct_path_sample per channel (resample.py:115-119).  Draws come
+   from device Philox streams unless the batch carries oracle draws. */
+int frir_simulate(const frir_plan* plan, const frir_batch* batch, void* workspace,
+                  size_t workspace_bytes, float* out_full, float* out_early,
+                  int32_t* direct_index, void* stream);
+
+/* Kernel launches frir_simulate issues for `batch` (for launch accounting). */
+int32_t frir_launch_count(const frir_plan* plan, const frir_batch* batch, int32_t early);
+
+const char* frir_last_error(void);
+int32_t frir_abi_version(void);
+/* sizeof of frir_job (0), frir_batch (1), frir_plan_desc (2): lets bindings
+   verify their struct mirrors. */
+int64_t frir_struct_size(int32_t which);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FRIR_H_ */

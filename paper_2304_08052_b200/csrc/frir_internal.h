@@ -1,0 +1,50 @@
+// Internal structures shared by the C-ABI layer and the kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/frir.h"
+#include "frir_design.h"
+
+namespace frir {
+
+constexpr int kWin = 32;        // outputs per gather window (one per lane)
+constexpr int kTileWin = 8;     // windows per LP-scan tile
+constexpr int kTile = kWin * kTileWin;
+constexpr int kChunk = kTile / 32;  // serial outputs per lane in the scan
+constexpr int kExt = 10;        // half2 / r_l: leading LP samples before output 0
+constexpr int kSpBias = 64;     // bias of the packed start index
+constexpr int kMaxRows = 17408; // max images + 1 per job (K2 block sort capacity)
+
+// Device-resident, read-only per-plan data (uploaded once by frir_plan_create).
+struct DevPlan {
+  frir_plan_desc d;
+  float2* comp;        // [r_h][sup] (TD, TW), phase-major
+  double* h1up;        // [len1]
+  double* ppow;        // [horizon][2]
+  double* zphase;      // [down][2]
+  double* kappa;       // [half2][2]
+  double* u;           // [half2]
+  double* scan;        // LP scan constants, see kernels (kScanDoubles)
+  double lp[6];        // c1, c2, v0
+};
+
+constexpr int kScanDoubles = 4 * 5 + 4 * 32 + 2 * kChunk;  // KS powers, M^(chunk*L), free response
+
+}  // namespace frir
+
+struct frir_plan {
+  frir::Design design;
+  frir::DevPlan dev;
+  int device;
+};
+
+namespace frir {
+void set_error(const std::string& msg);
+int launch_simulate(const frir_plan* plan, const frir_batch* b, void* ws, size_t ws_bytes,
+                    float* out_full, float* out_early, int32_t* direct_index, cudaStream_t st);
+size_t workspace_bytes(const frir_batch* b);
+int launches(const frir_batch* b, int early);
+}  // namespace frir

@@ -1,0 +1,195 @@
+"""Device engine: job tables -> libfrir -> device tensors.
+
+torch provides device memory and the current stream (plumbing only); all
+arithmetic runs in libfrir.so (csrc/).  One call renders a whole batch of
+(room, source) jobs; see DESIGN.md for the data layout.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _abi
+
+_plan_lock = threading.Lock()
+_plans: dict = {}
+
+
+class Plan:
+    """Per (sample_rate, device) filter tables resident on the GPU."""
+
+    def __init__(self, sample_rate: int, device: int):
+        self.sample_rate = int(sample_rate)
+        self.device = device
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            _abi.check(_abi.lib().frir_plan_create(self.sample_rate, ctypes.byref(handle)),
+                       "frir_plan_create")
+        self.handle = handle
+        self.desc = _abi.FrirPlanDesc()
+        _abi.check(_abi.lib().frir_plan_describe(handle, ctypes.byref(self.desc)), "frir_plan_describe")
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            if self.handle:
+                _abi.lib().frir_plan_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def get_plan(sample_rate: int, device=None) -> Plan:
+    if not torch.cuda.is_available():
+        raise _abi.FrirLibraryError("no CUDA device: the FRAM-RIR engine runs only on the GPU")
+    dev = torch.cuda.current_device() if device is None else torch.device(device).index
+    if dev is None:
+        dev = torch.cuda.current_device()
+    key = (int(sample_rate), dev)
+    with _plan_lock:
+        plan = _plans.get(key)
+        if plan is None:
+            plan = Plan(sample_rate, dev)
+            _plans[key] = plan
+    return plan
+
+
+def new_jobs(n: int) -> np.ndarray:
+    """Zeroed job table with the reference SimParams defaults."""
+    jobs = np.zeros(n, dtype=_abi.JOB_DTYPE)
+    jobs["c0"] = 343.0
+    jobs["alpha"] = 0.1
+    jobs["beta"] = 1.0
+    jobs["perturb_lo"] = -2.0
+    jobs["perturb_hi"] = 2.0
+    jobs["tau"] = 0.25
+    return jobs
+
+
+@dataclass
+class PreparedBatch:
+    """Host-side job table after frir_jobs_prepare (validated, laid out)."""
+
+    sample_rate: int
+    jobs: np.ndarray
+    mics: np.ndarray
+    chan_job: np.ndarray
+    chan_order: np.ndarray
+    batch: _abi.FrirBatch
+    padded: bool
+    draws: tuple | None = None
+
+    @property
+    def n_jobs(self) -> int:
+        return len(self.jobs)
+
+
+def prepare(sample_rate: int, jobs: np.ndarray, mics: np.ndarray, padded: bool = False,
+            draws=None) -> PreparedBatch:
+    """Validate and lay out a job table on the host (no GPU needed)."""
+    jobs = np.ascontiguousarray(jobs, dtype=_abi.JOB_DTYPE).copy()
+    mics = np.ascontiguousarray(mics, dtype=np.float64).reshape(-1, 3)
+    n_ch = int(jobs["n_mics"].sum()) if len(jobs) else 0
+    chan_job = np.zeros(n_ch, dtype=np.int32)
+    chan_order = np.zeros(n_ch, dtype=np.int32)
+    batch = _abi.FrirBatch()
+    _abi.check(
+        _abi.lib().frir_jobs_prepare(int(sample_rate), jobs.ctypes.data, len(jobs), int(bool(padded)),
+                                     ctypes.byref(batch), chan_job.ctypes.data,
+                                     chan_order.ctypes.data),
+        "frir_jobs_prepare",
+    )
+    if draws is not None:
+        draws = tuple(np.ascontiguousarray(d, dtype=np.float64) for d in draws)
+        if len(draws) != 4 or any(d.shape != (batch.total_images,) for d in draws):
+            raise ValueError("oracle draws must be 4 arrays of total_images rows")
+    return PreparedBatch(sample_rate, jobs, mics, chan_job, chan_order, batch, bool(padded), draws)
+
+
+@dataclass
+class BatchResult:
+    """Device outputs of one batch.
+
+    ``full``/``early`` are flat float32 tensors; channel ``m`` of job ``j`` is
+    ``full[jobs['out_off'][j] + m * jobs['out_stride'][j]:][:jobs['n2'][j]]``.
+    """
+
+    prepared: PreparedBatch
+    full: torch.Tensor
+    early: torch.Tensor | None
+    direct_index: torch.Tensor
+
+    def job_view(self, j: int, kind: str = "full") -> torch.Tensor:
+        J = self.prepared.jobs[j]
+        buf = self.full if kind == "full" else self.early
+        m, stride, n2, off = int(J["n_mics"]), int(J["out_stride"]), int(J["n2"]), int(J["out_off"])
+        return buf[off: off + m * stride].view(m, stride)[:, :n2]
+
+
+class DeviceBatch:
+    """Device-resident copy of a prepared batch plus its workspace."""
+
+    def __init__(self, pb: PreparedBatch, device=None, stream=None):
+        self.pb = pb
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index)
+        self.device = dev
+        self.plan = get_plan(pb.sample_rate, dev)
+        u8 = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.uint8).reshape(-1))
+        self.jobs = u8(pb.jobs).to(dev, non_blocking=False)
+        self.chan_job = torch.from_numpy(pb.chan_job).to(dev)
+        self.chan_order = torch.from_numpy(pb.chan_order).to(dev)
+        self.mics = torch.from_numpy(pb.mics.reshape(-1)).to(dev)
+        self.draws = None
+        if pb.draws is not None:
+            self.draws = [torch.from_numpy(d).to(dev) for d in pb.draws]
+        b = _abi.FrirBatch()
+        ctypes.memmove(ctypes.byref(b), ctypes.byref(pb.batch), ctypes.sizeof(b))
+        b.jobs = self.jobs.data_ptr()
+        b.chan_job = self.chan_job.data_ptr()
+        b.chan_order = self.chan_order.data_ptr()
+        b.mics = self.mics.data_ptr()
+        if self.draws is not None:
+            b.draw_dist, b.draw_az, b.draw_el, b.draw_refl = (d.data_ptr() for d in self.draws)
+        self.batch = b
+        ws = _abi.lib().frir_workspace_size(self.plan.handle, ctypes.byref(b))
+        self.workspace = torch.empty(int(ws), dtype=torch.uint8, device=dev)
+
+    def alloc_outputs(self, include_early: bool = True):
+        n = int(self.batch.total_out)
+        full = torch.empty(n, dtype=torch.float32, device=self.device)
+        early = torch.empty(n, dtype=torch.float32, device=self.device) if include_early else None
+        if self.pb.padded:
+            full.zero_()
+            if early is not None:
+                early.zero_()
+        direct = torch.empty(int(self.batch.total_channels), dtype=torch.int32, device=self.device)
+        return full, early, direct
+
+    def launch(self, full, early, direct, stream=None) -> None:
+        """Enqueue the render of the whole batch on `stream` (default: current)."""
+        st = torch.cuda.current_stream(self.device) if stream is None else stream
+        status = _abi.lib().frir_simulate(
+            self.plan.handle, ctypes.byref(self.batch), self.workspace.data_ptr(),
+            self.workspace.numel(), full.data_ptr(), early.data_ptr() if early is not None else None,
+            direct.data_ptr(), st.cuda_stream,
+        )
+        _abi.check(status, "frir_simulate")
+
+    def run(self, include_early: bool = True, stream=None) -> BatchResult:
+        full, early, direct = self.alloc_outputs(include_early)
+        self.launch(full, early, direct, stream)
+        return BatchResult(self.pb, full, early, direct)
+
+    def launch_count(self, include_early: bool = True) -> int:
+        return int(_abi.lib().frir_launch_count(self.plan.handle, ctypes.byref(self.batch),
+                                                int(include_early)))
+
+
+def simulate_jobs(sample_rate: int, jobs: np.ndarray, mics: np.ndarray, include_early: bool = True,
+                  draws=None, padded: bool = False, device=None) -> BatchResult:
+    """Validate, upload and render a job table; returns device tensors."""
+    pb = prepare(sample_rate, jobs, mics, padded=padded, draws=draws)
+    return DeviceBatch(pb, device=device).run(include_early)

@@ -1,0 +1,150 @@
+"""Write tests/golden/* by running the UNMODIFIED reference in place.
+
+    PYTHONPATH=/root/reference/pkg/src python tools/make_golden.py
+
+Imports ``framrir`` from /root/reference (read-only, never copied).  The
+fixtures are small (< 1 MB total) and committed; the GPU box never needs the
+reference.  Cases:
+
+* kat.json            numpy Philox/SeedSequence words, rate factors,
+                      reflection coefficients and SURVEY Appendix C values.
+* cfg1.npz            BASELINE config 1 (simulate_rir full + early, float32),
+                      its direct indices and the reference ImageSet draws.
+* cases.npz           small scenes over 8/16/22.05/44.1/48 kHz with their
+                      draws and reference outputs (float32) and FP64 peaks.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg/src")
+sys.path.insert(0, str(REF))
+import framrir as F  # noqa: E402
+from framrir.core import (  # noqa: E402
+    max_reflections,
+    reflection_coefficient,
+    sample_image_geometry,
+    sample_reflection_counts,
+)
+
+OUT = Path(__file__).resolve().parents[1] / "tests" / "golden"
+
+
+def cfg1_scene():
+    ctr = np.array([3.0, 2.5, 1.2])
+    src = np.array([2.0, 3.5, 1.5])
+    v = src - ctr
+    d = float(np.linalg.norm(v))
+    az = math.atan2(v[1], v[0])
+    el = math.asin(v[2] / d)
+    mics = F.linear_array([0.05, 0.05, 0.05])
+    return F.Scene(room_dims=(6.0, 5.0, 3.0), mic_positions=mics, sources=[(d, az, el)])
+
+
+def draws_of(params, scene, k):
+    im = sample_image_geometry(params, scene, k)
+    if params.num_images > 0:
+        r = reflection_coefficient(scene.room_dims, params.t60)
+        rr = max_reflections(params.t60, im.direct_distance, r, params.sound_speed)
+        im = sample_reflection_counts(im, params, rr)
+    return im
+
+
+def kat():
+    out = {"philox": [], "rate_factors": {}, "reflection": []}
+    for seed, k, stage, first in [(0, 0, 0, 0), (17, 2, 1, 5), (2**63 - 5, 1, 0, 1021),
+                                  (123456789012, 0, 1, 3), (91, 0, 0, 4095)]:
+        g = np.random.Generator(np.random.Philox(np.random.SeedSequence((seed, k, stage))))
+        words = g.random(first + 8)[first:]
+        key = np.random.SeedSequence((seed, k, stage)).generate_state(2, np.uint64)
+        out["philox"].append({"seed": str(seed), "k": k, "stage": stage, "first": first,
+                              "doubles": [float(x).hex() for x in words],
+                              "key": [str(int(x)) for x in key]})
+    for fs in (8000, 11025, 16000, 22050, 24000, 32000, 44100, 48000, 96000):
+        f = F.rate_factors(fs)
+        out["rate_factors"][str(fs)] = [f.r_h, f.r_l]
+    for dims, t60 in [((5.0, 4.0, 3.0), 0.5), ((6.0, 5.0, 3.0), 0.5), ((8.0, 7.0, 3.5), 1.2)]:
+        out["reflection"].append({"dims": dims, "t60": t60,
+                                  "r": float(reflection_coefficient(dims, t60)).hex()})
+    p = F.SimParams(t60=0.5, num_images=2048, seed=0)
+    sc = cfg1_scene()
+    im = draws_of(p, sc, 0)
+    r = reflection_coefficient(sc.room_dims, 0.5)
+    out["cfg1"] = {
+        "r": float(r).hex(),
+        "rr_max": float(max_reflections(0.5, im.direct_distance, r)).hex(),
+        "direct_mic_distances": [float(x).hex() for x in im.mic_distances[0]],
+    }
+    return out
+
+
+def cfg1():
+    p = F.SimParams(t60=0.5, num_images=2048, seed=0)
+    sc = cfg1_scene()
+    res = F.simulate_rir(p, sc, include_early=True)[0]
+    im = draws_of(p, sc, 0)
+    np.savez_compressed(
+        OUT / "cfg1.npz",
+        full=res.full.samples.astype(np.float32), early=res.early.samples.astype(np.float32),
+        full_peak=np.abs(res.full.samples).max(axis=1), early_peak=np.abs(res.early.samples).max(axis=1),
+        direct=res.full.direct_path_sample.astype(np.int64),
+        dist=im.distances, az=im.azimuths, el=im.elevations, refl=im.reflections,
+        mic_distances=im.mic_distances, mics=np.asarray(sc.mic_positions, float),
+        source=np.asarray(sc.sources, float), room=np.asarray(sc.room_dims, float),
+    )
+
+
+CASES = [
+    # fs, t60, images, seed, mics spacings, source (d, az, el), room
+    (16000, 0.1, 256, 3, [0.04, 0.08, 0.04], (1.5, 0.3, 0.1), (5.0, 4.0, 3.0)),
+    (16000, 0.25, 64, 11, [0.08], (1.2, 0.0, 0.0), (5.0, 4.0, 3.0)),
+    (16000, 0.05, 32, 5, [0.05], (0.9, 2.0, -0.3), (4.0, 3.5, 2.8)),
+    (16000, 0.15, 0, 7, [0.05, 0.05], (2.0, 1.0, 0.0), (6.0, 5.0, 3.0)),
+    (8000, 0.2, 200, 13, [0.1], (1.7, 4.0, 0.2), (7.0, 6.0, 3.0)),
+    (22050, 0.12, 300, 17, [0.03, 0.03], (1.1, 5.5, 0.0), (5.0, 5.0, 3.0)),
+    (44100, 0.08, 400, 19, [0.02], (1.4, 0.7, 0.4), (6.0, 4.0, 3.0)),
+    (48000, 0.06, 512, 23, [0.04, 0.04], (1.2, 3.3, -0.2), (9.0, 8.0, 4.0)),
+]
+
+
+def cases():
+    blobs = {}
+    meta = []
+    for ci, (fs, t60, n, seed, sp, src, room) in enumerate(CASES):
+        p = F.SimParams(t60=t60, sample_rate=fs, num_images=n, seed=seed)
+        sc = F.Scene(room_dims=room, mic_positions=F.linear_array(sp), sources=[src])
+        res = F.simulate_rir(p, sc, include_early=True)[0]
+        im = draws_of(p, sc, 0)
+        pre = f"c{ci}_"
+        blobs[pre + "full"] = res.full.samples.astype(np.float32)
+        blobs[pre + "early"] = res.early.samples.astype(np.float32)
+        blobs[pre + "peak"] = np.array([np.abs(res.full.samples).max(), np.abs(res.early.samples).max()])
+        blobs[pre + "direct"] = res.full.direct_path_sample.astype(np.int64)
+        blobs[pre + "dist"] = im.distances
+        blobs[pre + "az"] = im.azimuths
+        blobs[pre + "el"] = im.elevations
+        blobs[pre + "refl"] = im.reflections
+        blobs[pre + "mics"] = np.asarray(sc.mic_positions, float)
+        meta.append({"fs": fs, "t60": t60, "num_images": n, "seed": seed, "spacings": sp,
+                     "source": list(src), "room": list(room)})
+    np.savez_compressed(OUT / "cases.npz", **blobs)
+    (OUT / "cases.json").write_text(json.dumps(meta, indent=1))
+
+
+def main():
+    OUT.mkdir(parents=True, exist_ok=True)
+    (OUT / "kat.json").write_text(json.dumps(kat(), indent=1))
+    cfg1()
+    cases()
+    for f in sorted(OUT.iterdir()):
+        print(f.name, f.stat().st_size)
+
+
+if __name__ == "__main__":
+    main()
