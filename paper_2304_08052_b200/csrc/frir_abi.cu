@@ -131,7 +131,11 @@ int frir_plan_create(int32_t fs, frir_plan** out) {
   frir_plan* p = new frir_plan();
   std::string err;
   if (!design(fs, &p->design, &err)) { delete p; set_error(err); return FRIR_EINVAL; }
-  if (p->design.d.r_h > 1023) { delete p; set_error("sample_rate below 1 kHz is not supported"); return FRIR_ERANGE; }
+  if ((long)p->design.d.r_h * p->design.d.sup >= 4096) {
+    delete p;
+    set_error("sample_rate " + std::to_string(fs) + " is below the supported range (phase table too large)");
+    return FRIR_ERANGE;
+  }
   const Design& D = p->design;
   DevPlan& dv = p->dev;
   std::memset(&dv, 0, sizeof dv);

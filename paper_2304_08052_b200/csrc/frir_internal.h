@@ -11,7 +11,7 @@
 namespace frir {
 
 constexpr int kWin = 32;        // outputs per gather window (one per lane)
-constexpr int kTileWin = 8;     // windows per LP-scan tile
+constexpr int kTileWin = 4;     // windows per LP-scan tile
 constexpr int kTile = kWin * kTileWin;
 constexpr int kChunk = kTile / 32;  // serial outputs per lane in the scan
 constexpr int kExt = 10;        // half2 / r_l: leading LP samples before output 0

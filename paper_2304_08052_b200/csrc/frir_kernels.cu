@@ -29,6 +29,7 @@ struct Workspace {
   double* pz;
   double* lg;
   int2* items;
+  int* chan_q0;
   int* counter;
 };
 
@@ -43,6 +44,7 @@ Workspace carve(void* base, const frir_batch* b) {
   w.pz = (double*)p; p += align_up(ni * 8);
   w.lg = (double*)p; p += align_up(ni * 8);
   w.items = (int2*)p; p += align_up((size_t)b->total_items * 8);
+  w.chan_q0 = (int*)p; p += align_up((size_t)b->total_channels * 4);
   w.counter = (int*)p;
   return w;
 }
@@ -157,6 +159,7 @@ struct DelayArgs {
 __device__ __forceinline__ int ceil_div_i(int a, int b) {  // b > 0, any sign of a
   return a >= 0 ? (a + b - 1) / b : -((-a) / b);
 }
+__device__ __forceinline__ int ceil_div_d(int a, int b) { return ceil_div_i(a, b); }
 
 template <int THREADS, int IPT>
 __global__ void __launch_bounds__(THREADS) delay_kernel(DelayArgs A) {
@@ -200,6 +203,7 @@ __global__ void __launch_bounds__(THREADS) delay_kernel(DelayArgs A) {
   __syncthreads();
   const int q0 = s_q0;
   if (threadIdx.x == 0) {
+    A.ws.chan_q0[c] = q0;
     // resample.py:115-119 direct = clip(round(q0 / r_h), 0, n2 - 1), half-even
     double dv = rint(__ddiv_rn((double)q0, (double)r_h));
     int di = (int)dv;
@@ -213,12 +217,13 @@ __global__ void __launch_bounds__(THREADS) delay_kernel(DelayArgs A) {
     int r = threadIdx.x * IPT + k;
     if (r < rows) {
       int rel = q[k] - q0;
-      uint32_t early = (rel >= -lo && rel <= hi) ? 1u : 0u;  // core.py:259-264
+      bool early = rel >= -lo && rel <= hi;  // core.py:259-264
       int s = ceil_div_i(q[k] + t0, r_h);
-      int sp = s + kExt;
-      uint32_t phi = (uint32_t)(r_h * s - q[k] - t0);
-      key[k] = (uint32_t)(sp > 0 ? sp : 0) >> 5;
-      val[k] = make_uint2((uint32_t)(sp + kSpBias) | (phi << 20) | (early << 30), __float_as_uint(a[k]));
+      uint32_t spb = (uint32_t)(s + kExt + kSpBias);  // biased output-rate start, >= 0
+      uint32_t off = (uint32_t)((r_h * s - q[k] - t0) * A.d.sup);  // phase row offset
+      key[k] = spb >> 5;
+      // early flag rides in the sign of the (positive) gain
+      val[k] = make_uint2(spb | (off << 20), __float_as_uint(early ? -a[k] : a[k]));
     } else {
       key[k] = 0xffffffffu;
       val[k] = make_uint2(0u, 0u);
@@ -303,14 +308,68 @@ __device__ __forceinline__ void lp_scan_tile(double* buf, const double* scan, do
   s1 = shfl_d(l[kChunk - 2], 31);
 }
 
+// Accumulate window w (outputs n' in [32w, 32w + 32), one per lane) from the
+// bucket-sorted items.  Items are staged 32 at a time through per-warp shared
+// memory and read back as broadcasts; each candidate costs one table LDS.64
+// and two (four in early windows) FFMAs per lane.  Returns the new lower item
+// bound for window w + 1.
+template <bool EW>
+__device__ __forceinline__ int gather_window(const int2* __restrict__ items, int rows, int plo,
+                                             int w, int nb, int lane, int sup,
+                                             const float2* __restrict__ s_comp, int2* s_it,
+                                             float& accD, float& accW, float& accDe,
+                                             float& accWe) {
+  const int nbb = w * kWin + lane + kSpBias;  // biased output index of this lane
+  const unsigned wb = (unsigned)(w + 2);      // biased bucket of window w
+  const unsigned lowb = (unsigned)(w + 3 - nb);
+  int p = plo, newlo = -1;
+  for (;;) {
+    const int pi = p + lane;
+    int2 mine = pi < rows ? items[pi] : make_int2(0x7FFFFFFF, 0);
+    const unsigned bk = ((unsigned)mine.x & 0xFFFFFu) >> 5;
+    const bool inwin = pi < rows && bk <= wb;
+    const unsigned take = __ballot_sync(0xffffffffu, inwin);
+    const unsigned keep = __ballot_sync(0xffffffffu, pi < rows && bk >= lowb);
+    if (newlo < 0 && keep) newlo = p + __ffs(keep) - 1;
+    __syncwarp();
+    s_it[lane] = mine;
+    __syncwarp();
+    const int cnt = __popc(take);
+#pragma unroll 4
+    for (int jj = 0; jj < cnt; ++jj) {
+      const int2 it = s_it[jj];
+      const int idx = nbb - (it.x & 0xFFFFF);
+      if ((unsigned)idx < (unsigned)sup) {
+        const float2 t = s_comp[((unsigned)it.x >> 20) + idx];
+        const float ae = __int_as_float(it.y);
+        accD = fmaf(fabsf(ae), t.x, accD);
+        accW = fmaf(fabsf(ae), t.y, accW);
+        if (EW) {
+          const float e = fmaxf(-ae, 0.f);
+          accDe = fmaf(e, t.x, accDe);
+          accWe = fmaf(e, t.y, accWe);
+        }
+      }
+    }
+    if (cnt < 32) {
+      p += cnt;
+      break;
+    }
+    p += 32;
+  }
+  __syncwarp();
+  return newlo >= 0 ? newlo : p;
+}
+
 template <bool EARLY>
-__global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
+__global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const frir_plan_desc& d = A.plan.d;
   const int ncomp = d.r_h * d.sup;
   float2* s_comp = reinterpret_cast<float2*>(smem);
   double* s_scan = reinterpret_cast<double*>(smem + ((ncomp * 8 + 15) & ~15));
   double* s_warp = s_scan + kScanDoubles;
+  int2* s_items = reinterpret_cast<int2*>(s_warp + (size_t)kWarps * (EARLY ? 2 : 1) * kWarpBuf);
   for (int i = threadIdx.x; i < ncomp; i += blockDim.x) s_comp[i] = A.plan.comp[i];
   for (int i = threadIdx.x; i < kScanDoubles; i += blockDim.x) s_scan[i] = A.plan.scan[i];
   __syncthreads();
@@ -318,6 +377,9 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* bufF = s_warp + (size_t)warp * (EARLY ? 2 : 1) * kWarpBuf;
   double* bufE = bufF + kWarpBuf;
+  int2* s_it = s_items + 32 * warp;
+  const int d_lo = (6 * d.r_h * d.sample_rate + 999) / 1000;   // core.py:257
+  const int d_hi = (50 * d.r_h * d.sample_rate + 999) / 1000;  // core.py:258
   const double c1 = A.plan.lp[0], c2 = A.plan.lp[1];
   const Cplx v0a = {A.plan.lp[2], A.plan.lp[3]}, v0b = {A.plan.lp[4], A.plan.lp[5]};
   const int sup = d.sup, nb = d.nb, r_h = d.r_h, up = d.up, down = d.down, half1 = d.half1;
@@ -350,9 +412,10 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
         if (r >= 0) {
           int2 it = items[r];
           int sp = (it.x & 0xFFFFF) - kSpBias;
-          int phi = (it.x >> 20) & 0x3FF;
-          early = (it.x >> 30) & 1;
-          a = __int_as_float(it.y);
+          int phi = ((unsigned)it.x >> 20) / sup;
+          float ae = __int_as_float(it.y);
+          early = ae < 0.f;
+          a = fabsf(ae);
           q = r_h * (sp - kExt) - d.t0 - phi;
           long e = (long)up * q + half1;
           khi = e >= 0 ? e / down : -((-e + down - 1) / down);
@@ -453,7 +516,11 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
 
     // ---- main sweep over 32-sample windows in tiles of kTileWin
     const int nwin = (n2 + kExt + kWin - 1) / kWin;
-    int plo = 0;  // first item whose bucket >= w - nb
+    // early images have q in [q0 - lo, q0 + hi] (core.py:257-264): their starts
+    const int q0 = A.ws.chan_q0[c];
+    const int spe_lo = ceil_div_d(q0 - d_lo + d.t0, r_h) + kExt;
+    const int spe_hi = ceil_div_d(q0 + d_hi + d.t0, r_h) + kExt;
+    int plo = 0;  // first item whose bucket may still feed the current window
     double sF0 = 0.0, sF1 = 0.0, sE0 = 0.0, sE1 = 0.0;
     for (int w0 = 0; w0 < nwin; w0 += kTileWin) {
       float accD[kTileWin], accW[kTileWin], accDe[kTileWin], accWe[kTileWin];
@@ -461,33 +528,15 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
       for (int wi = 0; wi < kTileWin; ++wi) {
         accD[wi] = 0.f; accW[wi] = 0.f; accDe[wi] = 0.f; accWe[wi] = 0.f;
         const int w = w0 + wi;
+        const int n0 = w * kWin;
+        const bool ewin = EARLY && spe_lo <= n0 + 31 && spe_hi >= n0 - sup + 1;
         if (w < nwin) {
-          const int n0 = w * kWin;
-          const int nbase = n0 + lane;
-          int p = plo;
-          int newlo = -1;
-          const int lowb = w + 1 - nb;
-          for (; p < rows; ++p) {
-            const int2 it = items[p];
-            const int sp = (it.x & 0xFFFFF) - kSpBias;
-            const int bucket = (sp > 0 ? sp : 0) >> 5;
-            if (bucket > w) break;
-            if (newlo < 0 && bucket >= lowb) newlo = p;
-            if (sp + sup <= n0) continue;
-            const int idx = nbase - sp;
-            if ((unsigned)idx < (unsigned)sup) {
-              const int phi = (it.x >> 20) & 0x3FF;
-              const float a = __int_as_float(it.y);
-              const float2 t = s_comp[phi * sup + idx];
-              accD[wi] = fmaf(a, t.x, accD[wi]);
-              accW[wi] = fmaf(a, t.y, accW[wi]);
-              if (EARLY && (it.x & (1 << 30))) {
-                accDe[wi] = fmaf(a, t.x, accDe[wi]);
-                accWe[wi] = fmaf(a, t.y, accWe[wi]);
-              }
-            }
-          }
-          plo = newlo >= 0 ? newlo : p;
+          if (ewin)
+            plo = gather_window<true>(items, rows, plo, w, nb, lane, sup, s_comp, s_it,
+                                      accD[wi], accW[wi], accDe[wi], accWe[wi]);
+          else
+            plo = gather_window<false>(items, rows, plo, w, nb, lane, sup, s_comp, s_it,
+                                       accD[wi], accW[wi], accDe[wi], accWe[wi]);
         }
         bufF[pidx(wi * kWin + lane)] = (double)accW[wi];
         if (EARLY) bufE[pidx(wi * kWin + lane)] = (double)accWe[wi];
@@ -528,12 +577,14 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
 // ---------------------------------------------------------------- host launcher
 size_t workspace_bytes(const frir_batch* b) {
   size_t ni = (size_t)b->total_images;
-  return 4 * align_up(ni * 8) + align_up((size_t)b->total_items * 8) + 256;
+  return 4 * align_up(ni * 8) + align_up((size_t)b->total_items * 8) +
+         align_up((size_t)b->total_channels * 4) + 256;
 }
 
 static size_t render_smem(const frir_plan_desc& d, bool early) {
   size_t comp = ((size_t)d.r_h * d.sup * 8 + 15) & ~(size_t)15;
-  return comp + kScanDoubles * 8 + (size_t)kWarps * (early ? 2 : 1) * kWarpBuf * 8;
+  return comp + kScanDoubles * 8 + (size_t)kWarps * (early ? 2 : 1) * kWarpBuf * 8 +
+         (size_t)kWarps * 32 * 8;
 }
 
 template <int T, int IPT>

@@ -42,9 +42,15 @@ class Plan:
             pass
 
 
-def get_plan(sample_rate: int, device=None) -> Plan:
+def require_cuda() -> None:
+    """The engine has no CPU path: fail loudly without a GPU or the library."""
+    _abi.lib()
     if not torch.cuda.is_available():
         raise _abi.FrirLibraryError("no CUDA device: the FRAM-RIR engine runs only on the GPU")
+
+
+def get_plan(sample_rate: int, device=None) -> Plan:
+    require_cuda()
     dev = torch.cuda.current_device() if device is None else torch.device(device).index
     if dev is None:
         dev = torch.cuda.current_device()
@@ -133,6 +139,7 @@ class DeviceBatch:
     """Device-resident copy of a prepared batch plus its workspace."""
 
     def __init__(self, pb: PreparedBatch, device=None, stream=None):
+        require_cuda()
         self.pb = pb
         dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index)
         self.device = dev

@@ -1,0 +1,40 @@
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+TESTS = Path(__file__).resolve().parent
+if str(TESTS) not in sys.path:
+    sys.path.insert(0, str(TESTS))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
+    config.addinivalue_line("markers", "slow: long-running")
+
+
+@pytest.fixture(scope="session")
+def golden():
+    import json
+
+    import numpy as np
+
+    g = ROOT / "tests" / "golden"
+    return {
+        "kat": json.loads((g / "kat.json").read_text()),
+        "cfg1": dict(np.load(g / "cfg1.npz")),
+        "cases": dict(np.load(g / "cases.npz")),
+        "cases_meta": json.loads((g / "cases.json").read_text()),
+    }
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _built_library():
+    # Tests run against the in-tree library; build it if sources changed
+    # (nvcc cross-compiles without a GPU).
+    from paper_2304_08052_b200 import build
+
+    build.build()

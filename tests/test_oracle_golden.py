@@ -1,0 +1,94 @@
+"""Pin the CPU oracle (oracle/framrir_port.py) to the reference's own outputs.
+
+The fixtures come from running the unmodified reference
+(tools/make_golden.py); the reference's tests hold no stored vectors, so
+these plus its closed-form KATs (test_core.py) are the parity anchor.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import framrir_port as P
+
+
+def _case_job(golden, ci):
+    m = golden["cases_meta"][ci]
+    mics = golden["cases"][f"c{ci}_mics"]
+    return P.Job(room=tuple(m["room"]), mics=mics, center=mics.mean(axis=0),
+                  source=tuple(m["source"]), t60=m["t60"], sample_rate=m["fs"],
+                  num_images=m["num_images"], seed=m["seed"])
+
+
+def test_philox_stream_kat(golden):
+    # numpy Philox4x64-10 + SeedSequence as the reference keys them (core.py:86-91)
+    for e in golden["kat"]["philox"]:
+        g = P._gen(int(e["seed"]), e["k"], e["stage"])
+        got = g.random(e["first"] + 8)[e["first"]:]
+        assert [float(x).hex() for x in got] == e["doubles"]
+
+
+def test_rate_factors_kat(golden):
+    for fs, (r_h, r_l) in golden["kat"]["rate_factors"].items():
+        assert P.factors(int(fs)) == (r_h, r_l)
+
+
+def test_reflection_coefficient_kat(golden):
+    for e in golden["kat"]["reflection"]:
+        assert P.wall_reflection(e["dims"], e["t60"]) == float.fromhex(e["r"])
+    # test_core.py:32-35 closed form
+    assert P.wall_reflection((5.0, 4.0, 3.0), 0.5) == pytest.approx(0.98279, abs=1e-5)
+
+
+def test_rr_limit_kat():
+    # test_core.py:90-93
+    r = P.wall_reflection((5.0, 4.0, 3.0), 0.5)
+    assert P.rr_limit(0.5, 1.5, r, 343.0) == pytest.approx(124.896, abs=0.01)
+
+
+def test_cfg1_matches_reference(golden):
+    g = golden["cfg1"]
+    job = P.Job(room=tuple(g["room"]), mics=g["mics"], center=g["mics"].mean(axis=0),
+                source=tuple(g["source"][0]), t60=0.5, num_images=2048, seed=0)
+    full, early, direct = P.render(job)
+    assert np.array_equal(direct, g["direct"])
+    for m in range(4):
+        assert np.abs(full[m] - g["full"][m]).max() / g["full_peak"][m] < 1e-6
+        assert np.abs(early[m] - g["early"][m]).max() / g["early_peak"][m] < 1e-6
+    # direct arrivals and peak
+    assert list(direct) == [65, 67, 68, 70]
+    assert np.abs(full).max() == pytest.approx(1.122455176007e-02, rel=1e-10)
+
+
+def test_cfg1_draws_match_reference(golden):
+    g = golden["cfg1"]
+    job = P.Job(room=tuple(g["room"]), mics=g["mics"], center=g["mics"].mean(axis=0),
+                source=tuple(g["source"][0]), t60=0.5, num_images=2048, seed=0)
+    d = P.draw(job)
+    for name, key in (("distances", "dist"), ("azimuths", "az"), ("elevations", "el"),
+                      ("reflections", "refl")):
+        assert np.array_equal(getattr(d, name), g[key]), name
+    P.delays_gains(job, d)
+    assert np.array_equal(d.mic_distances, g["mic_distances"])
+
+
+@pytest.mark.parametrize("ci", range(8))
+def test_cases_match_reference(golden, ci):
+    job = _case_job(golden, ci)
+    full, early, direct = P.render(job)
+    pk = golden["cases"][f"c{ci}_peak"]
+    assert np.array_equal(direct, golden["cases"][f"c{ci}_direct"])
+    assert np.abs(full - golden["cases"][f"c{ci}_full"]).max() / pk[0] < 1e-6
+    assert np.abs(early - golden["cases"][f"c{ci}_early"]).max() / pk[1] < 1e-6
+
+
+def test_early_window_offsets():
+    # test_core.py:282-285
+    rate = 62 * 16000
+    assert -(-6 * rate // 1000) == 5952 and -(-50 * rate // 1000) == 49600
+
+
+def test_index_arithmetic():
+    # test_core.py:210-212
+    assert math.ceil(3.43 / 343.0 * 62 * 16000) == 9920

@@ -76,6 +76,33 @@ def kat():
     sc = cfg1_scene()
     im = draws_of(p, sc, 0)
     r = reflection_coefficient(sc.room_dims, 0.5)
+    from framrir.params import scene_fingerprint
+
+    def summary(params, scene):
+        res = F.simulate_rir(params, scene, include_early=True)
+        return [{
+            "full_energy": [float(v).hex() for v in (x.full.samples ** 2).sum(axis=1)],
+            "early_energy": [float(v).hex() for v in (x.early.samples ** 2).sum(axis=1)],
+            "full_peak": float(np.abs(x.full.samples).max()).hex(),
+            "direct": [int(v) for v in x.full.direct_path_sample],
+            "shape": list(x.full.samples.shape),
+            "metadata": {k: (v if not isinstance(v, float) else float(v).hex())
+                         for k, v in x.full.metadata.items()},
+        } for x in res]
+
+    # binding/tests/test_binding.py:15-22 configuration
+    bind_scene = F.Scene(room_dims=(5.0, 4.0, 3.0), mic_positions=F.linear_array([0.04, 0.08, 0.04]),
+                         sources=[(1.5, 0.5235987755982988, 0.0)])
+    out["binding"] = summary(F.SimParams(t60=0.3, num_images=256, seed=17), bind_scene)
+    # CLI KAT (pkg/test_output.txt:136): simulate --t60 0.25 --images 64 --seed 11 --source 1.2,0,0
+    cli_scene = F.Scene(room_dims=(5.0, 4.0, 3.0), mic_positions=F.linear_array([0.04, 0.08, 0.04]),
+                        sources=[(1.2, 0.0, 0.0)])
+    out["cli"] = summary(F.SimParams(t60=0.25, num_images=64, seed=11), cli_scene)
+    # two sources, multi-source ordering and per-source streams
+    two = F.Scene(room_dims=(6.0, 5.0, 3.0), mic_positions=F.linear_array([0.04, 0.08, 0.04]),
+                  sources=[(1.0, 0.5, 0.0), (2.0, 2.0, 0.1)])
+    out["two_sources"] = summary(F.SimParams(t60=0.2, num_images=512, seed=3), two)
+    out["fingerprints"] = {"cfg1": scene_fingerprint(sc), "binding": scene_fingerprint(bind_scene)}
     out["cfg1"] = {
         "r": float(r).hex(),
         "rr_max": float(max_reflections(0.5, im.direct_distance, r)).hex(),
