@@ -170,6 +170,17 @@ int frir_simulate(const frir_plan* plan, const frir_batch* batch, void* workspac
                   size_t workspace_bytes, float* out_full, float* out_early,
                   int32_t* direct_index, void* stream);
 
+/* frir_simulate split into its stages (bit 0: sampling/geometry K1, bit 1:
+   delays + per-channel sort K2, bit 2: render K3); stages must run in order on
+   one stream with the same workspace.  Lets callers time the render kernel. */
+#define FRIR_STAGE_GEOM 1
+#define FRIR_STAGE_DELAY 2
+#define FRIR_STAGE_RENDER 4
+#define FRIR_STAGE_ALL 7
+int frir_simulate_stages(const frir_plan* plan, const frir_batch* batch, void* workspace,
+                         size_t workspace_bytes, float* out_full, float* out_early,
+                         int32_t* direct_index, void* stream, int32_t stages);
+
 /* Kernel launches frir_simulate issues for `batch` (for launch accounting). */
 int32_t frir_launch_count(const frir_plan* plan, const frir_batch* batch, int32_t early);
 

@@ -16,6 +16,7 @@ import numpy as np
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libfrir.so"
 
 FRIR_OK, FRIR_EINVAL, FRIR_ECUDA, FRIR_ERANGE, FRIR_ENOMEM = 0, -1, -2, -3, -4
+STAGE_GEOM, STAGE_DELAY, STAGE_RENDER, STAGE_ALL = 1, 2, 4, 7
 TAB_H1, TAB_H2, TAB_SOS, TAB_COMP_D, TAB_COMP_W = 0, 1, 2, 3, 4
 TAB_KAPPA, TAB_U, TAB_ZPHASE, TAB_PPOW, TAB_LPCOEF = 5, 6, 7, 8, 9
 
@@ -79,6 +80,9 @@ SIGNATURES = [
     ("frir_simulate", c_int32,
      [c_void_p, ctypes.POINTER(FrirBatch), c_void_p, ctypes.c_size_t, c_void_p, c_void_p,
       c_void_p, c_void_p]),
+    ("frir_simulate_stages", c_int32,
+     [c_void_p, ctypes.POINTER(FrirBatch), c_void_p, ctypes.c_size_t, c_void_p, c_void_p,
+      c_void_p, c_void_p, c_int32]),
     ("frir_launch_count", c_int32, [c_void_p, ctypes.POINTER(FrirBatch), c_int32]),
     ("frir_last_error", ctypes.c_char_p, []),
     ("frir_abi_version", c_int32, []),

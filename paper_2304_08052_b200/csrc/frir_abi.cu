@@ -131,9 +131,9 @@ int frir_plan_create(int32_t fs, frir_plan** out) {
   frir_plan* p = new frir_plan();
   std::string err;
   if (!design(fs, &p->design, &err)) { delete p; set_error(err); return FRIR_EINVAL; }
-  if ((long)p->design.d.r_h * p->design.d.sup >= 4096) {
+  if (p->design.d.r_h > 1023 || p->design.d.sup > 64) {
     delete p;
-    set_error("sample_rate " + std::to_string(fs) + " is below the supported range (phase table too large)");
+    set_error("sample_rate " + std::to_string(fs) + " is outside the supported range (r_h <= 1023, <= 64 taps)");
     return FRIR_ERANGE;
   }
   const Design& D = p->design;
@@ -141,11 +141,13 @@ int frir_plan_create(int32_t fs, frir_plan** out) {
   std::memset(&dv, 0, sizeof dv);
   dv.d = D.d;
   cudaGetDevice(&p->device);
-  std::vector<float2> comp((size_t)D.d.r_h * D.d.sup);
+  // phase-major rows padded to 32 * ceil(sup / 32) taps (zeros past sup)
+  const int row = 32 * ((D.d.sup + 31) / 32);
+  std::vector<float2> comp((size_t)D.d.r_h * row, make_float2(0.f, 0.f));
   for (int ph = 0; ph < D.d.r_h; ++ph)
     for (int i = 0; i < D.d.sup; ++i) {
       size_t t = (size_t)ph + (size_t)D.d.r_h * i;  // t - t0
-      comp[(size_t)ph * D.d.sup + i] = make_float2((float)D.comp_d[t], (float)D.comp_w[t]);
+      comp[(size_t)ph * row + i] = make_float2((float)D.comp_d[t], (float)D.comp_w[t]);
     }
   std::vector<double> scan = scan_constants(D.d.c1, D.d.c2);
   cudaError_t e = cudaSuccess;
@@ -305,13 +307,15 @@ size_t frir_workspace_size(const frir_plan* plan, const frir_batch* b) {
   return workspace_bytes(b);
 }
 
-int frir_simulate(const frir_plan* plan, const frir_batch* b, void* ws, size_t ws_bytes,
-                  float* out_full, float* out_early, int32_t* direct_index, void* stream) {
+int frir_simulate_stages(const frir_plan* plan, const frir_batch* b, void* ws, size_t ws_bytes,
+                         float* out_full, float* out_early, int32_t* direct_index, void* stream,
+                         int32_t stages) {
   if (!plan || !b) { set_error("null argument"); return FRIR_EINVAL; }
   if (b->n_jobs > 0 && (!b->jobs || !b->chan_job || !b->mics || !out_full || !direct_index || !ws)) {
     set_error("null device pointer in batch");
     return FRIR_EINVAL;
   }
+  if (stages <= 0 || stages > FRIR_STAGE_ALL) { set_error("bad stage mask"); return FRIR_EINVAL; }
   const bool oracle = b->draw_dist || b->draw_az || b->draw_el || b->draw_refl;
   if (oracle && !(b->draw_dist && b->draw_az && b->draw_el && b->draw_refl)) {
     set_error("oracle mode needs all four draw arrays");
@@ -323,7 +327,14 @@ int frir_simulate(const frir_plan* plan, const frir_batch* b, void* ws, size_t w
     set_error("plan was created on device " + std::to_string(plan->device) + ", current device is " + std::to_string(dev));
     return FRIR_EINVAL;
   }
-  return launch_simulate(plan, b, ws, ws_bytes, out_full, out_early, direct_index, (cudaStream_t)stream);
+  return launch_simulate(plan, b, ws, ws_bytes, out_full, out_early, direct_index,
+                         (cudaStream_t)stream, stages);
+}
+
+int frir_simulate(const frir_plan* plan, const frir_batch* b, void* ws, size_t ws_bytes,
+                  float* out_full, float* out_early, int32_t* direct_index, void* stream) {
+  return frir_simulate_stages(plan, b, ws, ws_bytes, out_full, out_early, direct_index, stream,
+                              FRIR_STAGE_ALL);
 }
 
 int32_t frir_launch_count(const frir_plan* plan, const frir_batch* b, int32_t early) {

@@ -44,7 +44,8 @@ struct frir_plan {
 namespace frir {
 void set_error(const std::string& msg);
 int launch_simulate(const frir_plan* plan, const frir_batch* b, void* ws, size_t ws_bytes,
-                    float* out_full, float* out_early, int32_t* direct_index, cudaStream_t st);
+                    float* out_full, float* out_early, int32_t* direct_index, cudaStream_t st,
+                    int stages);
 size_t workspace_bytes(const frir_batch* b);
 int launches(const frir_batch* b, int early);
 }  // namespace frir

@@ -159,7 +159,6 @@ struct DelayArgs {
 __device__ __forceinline__ int ceil_div_i(int a, int b) {  // b > 0, any sign of a
   return a >= 0 ? (a + b - 1) / b : -((-a) / b);
 }
-__device__ __forceinline__ int ceil_div_d(int a, int b) { return ceil_div_i(a, b); }
 
 template <int THREADS, int IPT>
 __global__ void __launch_bounds__(THREADS) delay_kernel(DelayArgs A) {
@@ -220,7 +219,7 @@ __global__ void __launch_bounds__(THREADS) delay_kernel(DelayArgs A) {
       bool early = rel >= -lo && rel <= hi;  // core.py:259-264
       int s = ceil_div_i(q[k] + t0, r_h);
       uint32_t spb = (uint32_t)(s + kExt + kSpBias);  // biased output-rate start, >= 0
-      uint32_t off = (uint32_t)((r_h * s - q[k] - t0) * A.d.sup);  // phase row offset
+      uint32_t off = (uint32_t)(r_h * s - q[k] - t0);  // phase, < r_h <= 1023
       key[k] = spb >> 5;
       // early flag rides in the sign of the (positive) gain
       val[k] = make_uint2(spb | (off << 20), __float_as_uint(early ? -a[k] : a[k]));
@@ -313,63 +312,68 @@ __device__ __forceinline__ void lp_scan_tile(double* buf, const double* scan, do
 // memory and read back as broadcasts; each candidate costs one table LDS.64
 // and two (four in early windows) FFMAs per lane.  Returns the new lower item
 // bound for window w + 1.
-template <bool EW>
-__device__ __forceinline__ int gather_window(const int2* __restrict__ items, int rows, int plo,
-                                             int w, int nb, int lane, int sup,
-                                             const float2* __restrict__ s_comp, int2* s_it,
-                                             float& accD, float& accW, float& accDe,
-                                             float& accWe) {
-  const int nbb = w * kWin + lane + kSpBias;  // biased output index of this lane
-  const unsigned wb = (unsigned)(w + 2);      // biased bucket of window w
-  const unsigned lowb = (unsigned)(w + 3 - nb);
-  int p = plo, newlo = -1;
-  for (;;) {
-    const int pi = p + lane;
-    int2 mine = pi < rows ? items[pi] : make_int2(0x7FFFFFFF, 0);
-    const unsigned bk = ((unsigned)mine.x & 0xFFFFFu) >> 5;
-    const bool inwin = pi < rows && bk <= wb;
-    const unsigned take = __ballot_sync(0xffffffffu, inwin);
-    const unsigned keep = __ballot_sync(0xffffffffu, pi < rows && bk >= lowb);
-    if (newlo < 0 && keep) newlo = p + __ffs(keep) - 1;
-    __syncwarp();
-    s_it[lane] = mine;
-    __syncwarp();
-    const int cnt = __popc(take);
-#pragma unroll 4
-    for (int jj = 0; jj < cnt; ++jj) {
-      const int2 it = s_it[jj];
-      const int idx = nbb - (it.x & 0xFFFFF);
-      if ((unsigned)idx < (unsigned)sup) {
-        const float2 t = s_comp[((unsigned)it.x >> 20) + idx];
-        const float ae = __int_as_float(it.y);
-        accD = fmaf(fabsf(ae), t.x, accD);
-        accW = fmaf(fabsf(ae), t.y, accW);
-        if (EW) {
-          const float e = fmaxf(-ae, 0.f);
-          accDe = fmaf(e, t.x, accDe);
-          accWe = fmaf(e, t.y, accWe);
-        }
+// One warp renders one channel (full + optional early variant) in a single
+// ordered sweep over its bucket-sorted items.  Items of bucket b start in
+// output window b - 2 (n' = s' + k, biased by kSpBias = 64); each is visited
+// ONCE: lane L takes tap k = (L - delta) mod 32 (+32 j) of its phase row and
+// adds it to the window it lands in (accumulators a0, a1[, a2] for the current
+// and next windows).  When the sweep passes a bucket, the current window is
+// final and is emitted to the per-warp tile buffer; every kTileWin windows the
+// FP64 LP scan runs and y = D - LP is stored with coalesced writes.
+template <bool EARLY, int NBK>
+struct Channel {
+  // accumulators of windows w, w+1, w+2: D and W, full and early
+  float dF[NBK + 1], wF[NBK + 1], dE[NBK + 1], wE[NBK + 1];
+
+  __device__ __forceinline__ void clear() {
+#pragma unroll
+    for (int i = 0; i <= NBK; ++i) { dF[i] = 0.f; wF[i] = 0.f; dE[i] = 0.f; wE[i] = 0.f; }
+  }
+  __device__ __forceinline__ void shift() {
+#pragma unroll
+    for (int i = 0; i < NBK; ++i) { dF[i] = dF[i + 1]; wF[i] = wF[i + 1]; dE[i] = dE[i + 1]; wE[i] = wE[i + 1]; }
+    dF[NBK] = 0.f; wF[NBK] = 0.f; dE[NBK] = 0.f; wE[NBK] = 0.f;
+  }
+  // one item: x = biased start | phase << 20, ae = +-gain (sign = early flag).
+  // Lane L takes taps k0 + 32 j, k0 = (L - start) mod 32, of the item's phase
+  // row; they land in windows j (k0 <= L) or j + 1 (k0 > L).  Selects instead
+  // of branches keep the warp converged; only the early test branches, and
+  // it is warp-uniform.
+  template <bool EW>
+  __device__ __forceinline__ void add(int x, float ae, int lane, const float2* __restrict__ s_comp) {
+    const int k0 = (lane - x) & 31;
+    const int idx = ((((unsigned)x >> 20) & 0x3FF) << (5 + (NBK - 1))) | k0;
+    const bool hi = k0 > lane;
+    const float a = fabsf(ae);
+    const float alo = hi ? 0.f : a, ahi = hi ? a : 0.f;
+#pragma unroll
+    for (int j = 0; j < NBK; ++j) {
+      const float2 t = s_comp[idx + 32 * j];
+      dF[j] = fmaf(alo, t.x, dF[j]);
+      wF[j] = fmaf(alo, t.y, wF[j]);
+      dF[j + 1] = fmaf(ahi, t.x, dF[j + 1]);
+      wF[j + 1] = fmaf(ahi, t.y, wF[j + 1]);
+      if (EW && ae < 0.f) {
+        dE[j] = fmaf(alo, t.x, dE[j]);
+        wE[j] = fmaf(alo, t.y, wE[j]);
+        dE[j + 1] = fmaf(ahi, t.x, dE[j + 1]);
+        wE[j + 1] = fmaf(ahi, t.y, wE[j + 1]);
       }
     }
-    if (cnt < 32) {
-      p += cnt;
-      break;
-    }
-    p += 32;
   }
-  __syncwarp();
-  return newlo >= 0 ? newlo : p;
-}
+};
 
-template <bool EARLY>
-__global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A) {
+template <bool EARLY, int NBK>
+__global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const frir_plan_desc& d = A.plan.d;
-  const int ncomp = d.r_h * d.sup;
+  constexpr int kRow = 32 * NBK;
+  const int ncomp = d.r_h * kRow;
   float2* s_comp = reinterpret_cast<float2*>(smem);
-  double* s_scan = reinterpret_cast<double*>(smem + ((ncomp * 8 + 15) & ~15));
-  double* s_warp = s_scan + kScanDoubles;
-  int2* s_items = reinterpret_cast<int2*>(s_warp + (size_t)kWarps * (EARLY ? 2 : 1) * kWarpBuf);
+  double* s_scan = reinterpret_cast<double*>(smem + (size_t)ncomp * 8);
+  double* s_warp = s_scan + kScanDoubles;  // per warp: W buffers (F[, E])
+  float* s_dbuf = reinterpret_cast<float*>(s_warp + (size_t)kWarps * (EARLY ? 2 : 1) * kWarpBuf);
+  int2* s_items = reinterpret_cast<int2*>(s_dbuf + (size_t)kWarps * (EARLY ? 2 : 1) * kTile);
   for (int i = threadIdx.x; i < ncomp; i += blockDim.x) s_comp[i] = A.plan.comp[i];
   for (int i = threadIdx.x; i < kScanDoubles; i += blockDim.x) s_scan[i] = A.plan.scan[i];
   __syncthreads();
@@ -377,12 +381,13 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* bufF = s_warp + (size_t)warp * (EARLY ? 2 : 1) * kWarpBuf;
   double* bufE = bufF + kWarpBuf;
+  float* dbF = s_dbuf + (size_t)warp * (EARLY ? 2 : 1) * kTile;
+  float* dbE = dbF + kTile;
   int2* s_it = s_items + 32 * warp;
-  const int d_lo = (6 * d.r_h * d.sample_rate + 999) / 1000;   // core.py:257
-  const int d_hi = (50 * d.r_h * d.sample_rate + 999) / 1000;  // core.py:258
   const double c1 = A.plan.lp[0], c2 = A.plan.lp[1];
   const Cplx v0a = {A.plan.lp[2], A.plan.lp[3]}, v0b = {A.plan.lp[4], A.plan.lp[5]};
-  const int sup = d.sup, nb = d.nb, r_h = d.r_h, up = d.up, down = d.down, half1 = d.half1;
+  const int sup = d.sup, r_h = d.r_h, up = d.up, down = d.down, half1 = d.half1;
+  (void)sup;
 
   for (;;) {
     int ci = 0;
@@ -412,7 +417,7 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A)
         if (r >= 0) {
           int2 it = items[r];
           int sp = (it.x & 0xFFFFF) - kSpBias;
-          int phi = ((unsigned)it.x >> 20) / sup;
+          int phi = ((unsigned)it.x >> 20) & 0x3FF;
           float ae = __int_as_float(it.y);
           early = ae < 0.f;
           a = fabsf(ae);
@@ -514,61 +519,90 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A)
       }
     }
 
-    // ---- main sweep over 32-sample windows in tiles of kTileWin
+    // ---- ordered sweep: windows w = -2 .. nwin-1 over n' = n + 10
     const int nwin = (n2 + kExt + kWin - 1) / kWin;
-    // early images have q in [q0 - lo, q0 + hi] (core.py:257-264): their starts
-    const int q0 = A.ws.chan_q0[c];
-    const int spe_lo = ceil_div_d(q0 - d_lo + d.t0, r_h) + kExt;
-    const int spe_hi = ceil_div_d(q0 + d_hi + d.t0, r_h) + kExt;
-    int plo = 0;  // first item whose bucket may still feed the current window
+    Channel<EARLY, NBK> ch;
+    ch.clear();
     double sF0 = 0.0, sF1 = 0.0, sE0 = 0.0, sE1 = 0.0;
-    for (int w0 = 0; w0 < nwin; w0 += kTileWin) {
-      float accD[kTileWin], accW[kTileWin], accDe[kTileWin], accWe[kTileWin];
-#pragma unroll
-      for (int wi = 0; wi < kTileWin; ++wi) {
-        accD[wi] = 0.f; accW[wi] = 0.f; accDe[wi] = 0.f; accWe[wi] = 0.f;
-        const int w = w0 + wi;
-        const int n0 = w * kWin;
-        const bool ewin = EARLY && spe_lo <= n0 + 31 && spe_hi >= n0 - sup + 1;
-        if (w < nwin) {
-          if (ewin)
-            plo = gather_window<true>(items, rows, plo, w, nb, lane, sup, s_comp, s_it,
-                                      accD[wi], accW[wi], accDe[wi], accWe[wi]);
-          else
-            plo = gather_window<false>(items, rows, plo, w, nb, lane, sup, s_comp, s_it,
-                                       accD[wi], accW[wi], accDe[wi], accWe[wi]);
+    int w = -2;     // window that the front accumulators (index 0) hold
+    int slot = 0;   // next tile slot
+    auto emit = [&]() {
+      if (w >= 0) {
+        dbF[slot * kWin + lane] = ch.dF[0];
+        bufF[pidx(slot * kWin + lane)] = (double)ch.wF[0];
+        if (EARLY) {
+          dbE[slot * kWin + lane] = ch.dE[0];
+          bufE[pidx(slot * kWin + lane)] = (double)ch.wE[0];
         }
-        bufF[pidx(wi * kWin + lane)] = (double)accW[wi];
-        if (EARLY) bufE[pidx(wi * kWin + lane)] = (double)accWe[wi];
+        ++slot;
+        if (slot == kTileWin || w == nwin - 1) {
+          for (int s2 = slot; s2 < kTileWin; ++s2) {  // pad a partial last tile
+            bufF[pidx(s2 * kWin + lane)] = 0.0;
+            if (EARLY) bufE[pidx(s2 * kWin + lane)] = 0.0;
+          }
+          __syncwarp();
+          lp_scan_tile(bufF, s_scan, c1, c2, sF0, sF1, lane);
+          if (EARLY) lp_scan_tile(bufE, s_scan, c1, c2, sE0, sE1, lane);
+          __syncwarp();
+          const int w0 = w - slot + 1;
+          for (int wi = 0; wi < slot; ++wi) {
+            const int n = (w0 + wi) * kWin + lane - kExt;
+            const bool tailwin = (w0 + wi) * kWin - kExt + 31 >= n_c;  // warp-uniform
+            double cf = 0.0, ce = 0.0;
+            if (tailwin) {
+              int src = n - n_c;
+              src = src < 0 ? 0 : (src > 31 ? 31 : src);
+              cf = shfl_d(corrF, src);
+              if (EARLY) ce = shfl_d(corrE, src);
+            }
+            if (n >= 0 && n < n2) {
+              const bool fix = n >= n_c;
+              const double yf = (double)dbF[wi * kWin + lane] - bufF[pidx(wi * kWin + lane)] - (fix ? cf : 0.0);
+              outF[n] = (float)yf;
+              if (EARLY) {
+                const double ye = (double)dbE[wi * kWin + lane] - bufE[pidx(wi * kWin + lane)] - (fix ? ce : 0.0);
+                outE[n] = (float)ye;
+              }
+            }
+          }
+          __syncwarp();
+          slot = 0;
+        }
       }
+      ch.shift();
+      ++w;
+    };
+    for (int p = 0; p < rows; p += 32) {
+      const int pi = p + lane;
+      const int2 mine = pi < rows ? items[pi] : make_int2(0xFFFFF, 0);  // sentinel: last bucket
       __syncwarp();
-      lp_scan_tile(bufF, s_scan, c1, c2, sF0, sF1, lane);
-      if (EARLY) lp_scan_tile(bufE, s_scan, c1, c2, sE0, sE1, lane);
+      s_it[lane] = mine;
       __syncwarp();
-#pragma unroll
-      for (int wi = 0; wi < kTileWin; ++wi) {
-        const int np = (w0 + wi) * kWin + lane;  // n' = n + 10
-        const int n = np - kExt;
-        const bool tail = (w0 + wi) * kWin - kExt + 31 >= n_c;
-        double cf = 0.0, ce = 0.0;
-        if (tail) {  // warp-uniform
-          int src = n - n_c;
-          src = src < 0 ? 0 : (src > 31 ? 31 : src);
-          cf = shfl_d(corrF, src);
-          if (EARLY) ce = shfl_d(corrE, src);
-        }
-        if (n >= 0 && n < n2) {
-          const bool fix = n >= n_c;
-          double yf = (double)accD[wi] - bufF[pidx(wi * kWin + lane)] - (fix ? cf : 0.0);
-          outF[n] = (float)yf;
-          if (EARLY) {
-            double ye = (double)accDe[wi] - bufE[pidx(wi * kWin + lane)] - (fix ? ce : 0.0);
-            outE[n] = (float)ye;
+      const int bk = (mine.x & 0xFFFFF) >> 5;
+      const int cnt = min(32, rows - p);
+      const unsigned emask = EARLY ? __ballot_sync(0xffffffffu, pi < rows && mine.y < 0) : 0u;
+      int jj = 0;
+      while (jj < cnt) {  // runs of equal bucket (items are bucket-sorted)
+        const int b = __shfl_sync(0xffffffffu, bk, jj);
+        while (b > w + 2) emit();
+        const unsigned same = __ballot_sync(0xffffffffu, bk == b && lane < cnt);
+        const int end = 32 - __clz(same);
+        if (EARLY && (same & emask)) {
+#pragma unroll 2
+          for (; jj < end; ++jj) {
+            const int2 it = s_it[jj];
+            ch.template add<true>(it.x, __int_as_float(it.y), lane, s_comp);
+          }
+        } else {
+#pragma unroll 4
+          for (; jj < end; ++jj) {
+            const int2 it = s_it[jj];
+            ch.template add<false>(it.x, __int_as_float(it.y), lane, s_comp);
           }
         }
       }
-      __syncwarp();
     }
+    while (w < nwin) emit();
   }
 }
 
@@ -581,10 +615,30 @@ size_t workspace_bytes(const frir_batch* b) {
          align_up((size_t)b->total_channels * 4) + 256;
 }
 
+static int table_blocks(const frir_plan_desc& d) { return (d.sup + 31) / 32; }
+
 static size_t render_smem(const frir_plan_desc& d, bool early) {
-  size_t comp = ((size_t)d.r_h * d.sup * 8 + 15) & ~(size_t)15;
-  return comp + kScanDoubles * 8 + (size_t)kWarps * (early ? 2 : 1) * kWarpBuf * 8 +
-         (size_t)kWarps * 32 * 8;
+  const int v = early ? 2 : 1;
+  return (size_t)d.r_h * 32 * table_blocks(d) * 8 + kScanDoubles * 8 +
+         (size_t)kWarps * v * kWarpBuf * 8 + (size_t)kWarps * v * kTile * 4 + (size_t)kWarps * 32 * 8;
+}
+
+template <bool EARLY, int NBK>
+static cudaError_t launch_render(const RenderArgs& ra, const frir_plan_desc& d, long channels,
+                                 cudaStream_t st) {
+  size_t smem = render_smem(d, EARLY);
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e = cudaFuncSetAttribute(render_kernel<EARLY, NBK>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, render_kernel<EARLY, NBK>, kRenderThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  long want = (channels + kWarps - 1) / kWarps;
+  int grid = (int)std::min<long>((long)sms * per_sm, want);
+  render_kernel<EARLY, NBK><<<grid, kRenderThreads, smem, st>>>(ra);
+  return cudaGetLastError();
 }
 
 template <int T, int IPT>
@@ -605,7 +659,8 @@ int launches(const frir_batch* b, int early) {
 }
 
 int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_t ws_bytes,
-                    float* out_full, float* out_early, int32_t* direct_index, cudaStream_t st) {
+                    float* out_full, float* out_early, int32_t* direct_index, cudaStream_t st,
+                    int stages) {
   const frir_plan_desc& d = plan->dev.d;
   if (ws_bytes < workspace_bytes(b)) {
     set_error("workspace too small: need " + std::to_string(workspace_bytes(b)) + " bytes");
@@ -618,17 +673,17 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_
   }
   if (b->n_jobs == 0 || b->total_channels == 0) return FRIR_OK;
   Workspace ws = carve(wsp, b);
-  cudaError_t e = cudaMemsetAsync(ws.counter, 0, sizeof(int), st);
-  if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FRIR_ECUDA; }
+  cudaError_t e = cudaSuccess;
 
-  // K1
+  if (stages & FRIR_STAGE_GEOM) {  // K1
   int maxg = (b->max_rows - 1 + 3) / 4;
   dim3 g1(b->n_jobs, (maxg + 127) / 128 > 0 ? (maxg + 127) / 128 : 1);
   geom_kernel<<<g1, 128, 0, st>>>(b->jobs, b->draw_dist, b->draw_az, b->draw_el, b->draw_refl, ws);
   e = cudaGetLastError();
   if (e != cudaSuccess) { set_error(std::string("geom_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
+  }
 
-  // K2
+  if (stages & FRIR_STAGE_DELAY) {  // K2
   DelayArgs da;
   da.jobs = b->jobs; da.chan_job = b->chan_job; da.mics = b->mics; da.ws = ws;
   da.direct_index = direct_index; da.d = d;
@@ -643,31 +698,23 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_
   else if (rows <= 8704) e = launch_delay<512, 17>(da, grid, st);
   else e = launch_delay<1024, 17>(da, grid, st);
   if (e != cudaSuccess) { set_error(std::string("delay_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
+  }
 
-  // K3
+  if (stages & FRIR_STAGE_RENDER) {  // K3
+  e = cudaMemsetAsync(ws.counter, 0, sizeof(int), st);
+  if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FRIR_ECUDA; }
   RenderArgs ra;
   ra.jobs = b->jobs; ra.chan_job = b->chan_job; ra.chan_order = b->chan_order;
   ra.total_channels = b->total_channels; ra.ws = ws; ra.plan = plan->dev;
   ra.out_full = out_full; ra.out_early = out_early;
   const bool early = out_early != nullptr;
-  size_t smem = render_smem(d, early);
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (early) {
-    cudaFuncSetAttribute(render_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, render_kernel<true>, kRenderThreads, smem);
-  } else {
-    cudaFuncSetAttribute(render_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, render_kernel<false>, kRenderThreads, smem);
-  }
-  if (per_sm < 1) per_sm = 1;
-  long want = (long)(b->total_channels + kWarps - 1) / kWarps;
-  int grid3 = (int)std::min<long>((long)sms * per_sm, want);
-  if (early) render_kernel<true><<<grid3, kRenderThreads, smem, st>>>(ra);
-  else render_kernel<false><<<grid3, kRenderThreads, smem, st>>>(ra);
-  e = cudaGetLastError();
+  const int nbk = table_blocks(d);
+  if (nbk == 1) e = early ? launch_render<true, 1>(ra, d, b->total_channels, st)
+                          : launch_render<false, 1>(ra, d, b->total_channels, st);
+  else e = early ? launch_render<true, 2>(ra, d, b->total_channels, st)
+                 : launch_render<false, 2>(ra, d, b->total_channels, st);
   if (e != cudaSuccess) { set_error(std::string("render_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
+  }
   return FRIR_OK;
 }
 

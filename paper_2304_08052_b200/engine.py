@@ -175,15 +175,15 @@ class DeviceBatch:
         direct = torch.empty(int(self.batch.total_channels), dtype=torch.int32, device=self.device)
         return full, early, direct
 
-    def launch(self, full, early, direct, stream=None) -> None:
+    def launch(self, full, early, direct, stream=None, stages: int = _abi.STAGE_ALL) -> None:
         """Enqueue the render of the whole batch on `stream` (default: current)."""
         st = torch.cuda.current_stream(self.device) if stream is None else stream
-        status = _abi.lib().frir_simulate(
+        status = _abi.lib().frir_simulate_stages(
             self.plan.handle, ctypes.byref(self.batch), self.workspace.data_ptr(),
             self.workspace.numel(), full.data_ptr(), early.data_ptr() if early is not None else None,
-            direct.data_ptr(), st.cuda_stream,
+            direct.data_ptr(), st.cuda_stream, stages,
         )
-        _abi.check(status, "frir_simulate")
+        _abi.check(status, "frir_simulate_stages")
 
     def run(self, include_early: bool = True, stream=None) -> BatchResult:
         full, early, direct = self.alloc_outputs(include_early)
