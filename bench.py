@@ -204,19 +204,9 @@ def run_ours(args):
     variants = 2 if early else 1
 
     # ---- workload shard (global room indices -> identical content for any N)
-    if cfg == 5:
-        total = args.rooms or CONFIGS[5]["rooms"]
-        lo, hi = rank * total // world, (rank + 1) * total // world
-        chunk = args.chunk or 4096
-        shards = [(s, min(chunk, hi - s)) for s in range(lo, hi, chunk)]
-        scaling = "strong"
-    elif cfg == 1:
-        shards = [(0, 1)]
-        scaling = "weak"
-    else:
-        per = args.rooms or CONFIGS[cfg]["rooms"]
-        shards = [(rank * per, per)]
-        scaling = "weak"
+    from paper_2304_08052_b200.shard import shard_ranges
+
+    shards, scaling = shard_ranges(cfg, rank, world, args.rooms, args.chunk or 4096)
     batches = []
     for start, n in shards:
         w = workloads.config1() if cfg == 1 else workloads.build(cfg, n, start=start)
