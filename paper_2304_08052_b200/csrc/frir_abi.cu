@@ -141,14 +141,19 @@ int frir_plan_create(int32_t fs, frir_plan** out) {
   std::memset(&dv, 0, sizeof dv);
   dv.d = D.d;
   cudaGetDevice(&p->device);
-  // phase-major rows padded to 32 * ceil(sup / 32) taps (zeros past sup)
-  const int row = 32 * ((D.d.sup + 31) / 32);
+  // phase-major rows of ceil(sup / 32) blocks; block j holds taps 32 j .. 32 j + 31
+  // TWICE (64 entries, zeros past sup) so the render kernel indexes it without
+  // wrapping (csrc/frir_kernels.cu Channel::add)
+  const int nbk = (D.d.sup + 31) / 32, row = 64 * nbk;
   std::vector<float2> comp((size_t)D.d.r_h * row, make_float2(0.f, 0.f));
   for (int ph = 0; ph < D.d.r_h; ++ph)
-    for (int i = 0; i < D.d.sup; ++i) {
-      size_t t = (size_t)ph + (size_t)D.d.r_h * i;  // t - t0
-      comp[(size_t)ph * row + i] = make_float2((float)D.comp_d[t], (float)D.comp_w[t]);
-    }
+    for (int j = 0; j < nbk; ++j)
+      for (int e = 0; e < 64; ++e) {
+        int k = 32 * j + (e & 31);
+        if (k >= D.d.sup) continue;
+        size_t t = (size_t)ph + (size_t)D.d.r_h * k;  // t - t0
+        comp[(size_t)ph * row + 64 * j + e] = make_float2((float)D.comp_d[t], (float)D.comp_w[t]);
+      }
   std::vector<double> scan = scan_constants(D.d.c1, D.d.c2);
   cudaError_t e = cudaSuccess;
   if (e == cudaSuccess) e = upload(&dv.comp, comp.data(), comp.size());
@@ -257,6 +262,10 @@ int frir_jobs_prepare(int32_t sample_rate, frir_job* jobs, int32_t n_jobs, int32
     int64_t n1 = ceil_div64((int64_t)J.L * d.up, d.down);
     int64_t n2 = ceil_div64(n1, d.r_l);
     if (n2 + kExt + kSpBias + 64 >= (1 << 20)) { set_error(pre + "RIR too long for the packed layout"); return FRIR_ERANGE; }
+    if (((int64_t)J.L + 66LL * d.r_h) * d.r_h >= (1LL << 32)) {
+      set_error(pre + "RIR too long for the delay arithmetic");
+      return FRIR_ERANGE;
+    }
     J.n1 = (int32_t)n1;
     J.n2 = (int32_t)n2;
     int rows = J.n_images + 1;

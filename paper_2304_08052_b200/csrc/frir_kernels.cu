@@ -1,10 +1,11 @@
 // sm_100a kernels of the FRAM-RIR hot path.
 //
 //   K1 geom_kernel    per (job, 4 images): Philox draws (or oracle draws) ->
-//                     image position + r^g in FP64          core.py:131-221
-//   K2 delay_kernel   per channel (job, mic): FP64 distance -> integer delay q,
-//                     FP32 gain, early flag, output-rate start/phase; block
-//                     radix sort by 32-sample window          core.py:228-265
+//                     FP64 image position, r^g, then per mic the exact integer
+//                     delay q, FP32 gain and output-rate start/phase items
+//                                                             core.py:131-251
+//   K2 sort_kernel    per channel: early flags, stable counting sort of the
+//                     items by 32-sample output window        core.py:254-265
 //   K3 render_kernel  persistent warps, one channel at a time: gather the
 //                     composite decimation/low-pass tables into 32-sample
 //                     windows (FP32), FP64 output-rate LP scan, exact tail
@@ -24,10 +25,6 @@ constexpr double kHalfPi = 1.5707963267948966;     // np.pi / 2.0
 constexpr double kPi = 3.141592653589793;          // np.pi/2 - (-np.pi/2)
 
 struct Workspace {
-  double* px;
-  double* py;
-  double* pz;
-  double* lg;
   int2* items;
   int* chan_q0;
   int* counter;
@@ -38,18 +35,13 @@ __host__ __device__ inline size_t align_up(size_t x) { return (x + 255) & ~(size
 Workspace carve(void* base, const frir_batch* b) {
   char* p = (char*)base;
   Workspace w;
-  size_t ni = (size_t)b->total_images;
-  w.px = (double*)p; p += align_up(ni * 8);
-  w.py = (double*)p; p += align_up(ni * 8);
-  w.pz = (double*)p; p += align_up(ni * 8);
-  w.lg = (double*)p; p += align_up(ni * 8);
   w.items = (int2*)p; p += align_up((size_t)b->total_items * 8);
   w.chan_q0 = (int*)p; p += align_up((size_t)b->total_channels * 4);
   w.counter = (int*)p;
   return w;
 }
 
-// ---------------------------------------------------------------- K1 geometry
+// ---------------------------------------------------------------- K1 geometry + delays
 // numpy operation order is kept with explicit _rn intrinsics (no FMA
 // contraction): positions/distances feed the exact integer delays.
 __device__ __forceinline__ void image_position(const frir_job& J, double dist, double az,
@@ -62,49 +54,93 @@ __device__ __forceinline__ void image_position(const frir_job& J, double dist, d
   *z = __dadd_rn(J.center[2], __dmul_rn(dist, se));
 }
 
-__global__ void __launch_bounds__(128) geom_kernel(const frir_job* __restrict__ jobs,
-                                                   const double* __restrict__ draw_dist,
-                                                   const double* __restrict__ draw_az,
-                                                   const double* __restrict__ draw_el,
-                                                   const double* __restrict__ draw_refl,
-                                                   Workspace ws) {
+struct GeomArgs {
+  const frir_job* jobs;
+  const double* mics;
+  const double* draw_dist;
+  const double* draw_az;
+  const double* draw_el;
+  const double* draw_refl;
+  Workspace ws;
+  int32_t* direct_index;
+  int r_h, t0;
+  unsigned rh_magic;  // ceil(2^32 / r_h): exact floor division for n < 2^32 / r_h
+  double rate;        // r_h * fs
+};
+
+// Integer high-rate delay of core.py:242-243, q = min(ceil((D / c0) * rate), L - 1),
+// with D = sqrt(dx^2 + dy^2 + dz^2) summed x, y, z (params.py:170-171).  The
+// product D * (rate / c0) is within 3 ulp of the reference's (D / c0) * rate, so
+// unless it lies within 1e-14 (relative) of an integer the ceiling is the
+// same; the exact division runs only in that (practically never) case.
+__device__ __forceinline__ int delay_of(double px, double py, double pz, const double* mic,
+                                        double c0, double rate, double rate_c0, int L, double* D) {
+  const double dx = __dsub_rn(px, mic[0]), dy = __dsub_rn(py, mic[1]), dz = __dsub_rn(pz, mic[2]);
+  const double d = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+  *D = d;
+  double x = __dmul_rn(d, rate_c0);
+  double k = ceil(x);
+  const double eps = 1e-14 * x;
+  if (k - x < eps || x - (k - 1.0) < eps) k = ceil(__dmul_rn(__ddiv_rn(d, c0), rate));
+  return k >= (double)(L - 1) ? L - 1 : (int)k;
+}
+
+// Item of the (image, mic) pair: biased output-rate start s' + 64 (20 bits) and
+// the phase phi (10 bits) of the composite tables, gain in the second word.
+__device__ __forceinline__ int2 make_item(int q, float a, int r_h, int t0, unsigned magic) {
+  // s = ceil((q + t0) / r_h); n = q + t0 + 64 r_h >= 0 (q >= 0, -t0 < 64 r_h)
+  const unsigned n = (unsigned)(q + t0 + 64 * r_h + r_h - 1);
+  const int s = (int)__umulhi(n, magic) - 64;
+  const unsigned spb = (unsigned)(s + kExt + kSpBias);
+  const unsigned phi = (unsigned)(r_h * s - q - t0);
+  return make_int2((int)(spb | (phi << 20)), __float_as_int(a));
+}
+
+__global__ void __launch_bounds__(128) geom_kernel(GeomArgs A) {
   const int j = blockIdx.x;
-  const frir_job& J = jobs[j];
-  const int I = J.n_images;
+  const frir_job& J = A.jobs[j];
+  const int I = J.n_images, rows = I + 1, M = J.n_mics;
   const int g = blockIdx.y * blockDim.x + threadIdx.x;  // group of 4 images
   const int ngroups = (I + 3) / 4;
-  if (g == 0) {  // row 0: direct path (core.py:169, params.py:156-159)
+  const double* mics = A.mics + 3 * (size_t)J.mic_off;
+  const double rate_c0 = __ddiv_rn(A.rate, J.c0);
+  int2* items = A.ws.items + J.item_off;
+  if (g == 0) {  // row 0: direct path (core.py:169, params.py:156-159), r**0 = 1
     double x, y, z;
     image_position(J, J.d0, J.az, J.el, &x, &y, &z);
-    size_t o = (size_t)J.img_off;
-    ws.px[o] = x; ws.py[o] = y; ws.pz[o] = z;
-    ws.lg[o] = 1.0;  // r ** 0.0
+    for (int m = 0; m < M; ++m) {
+      double D;
+      int q = delay_of(x, y, z, mics + 3 * m, J.c0, A.rate, rate_c0, J.L, &D);
+      items[(size_t)m * rows] = make_item(q, (float)__drcp_rn(D), A.r_h, A.t0, A.rh_magic);
+      A.ws.chan_q0[J.chan_off + m] = q;
+      // resample.py:115-119: clip(round(q0 / r_h), 0, n2 - 1), half-even
+      int di = (int)rint(__ddiv_rn((double)q, (double)A.r_h));
+      A.direct_index[J.chan_off + m] = di < 0 ? 0 : (di > J.n2 - 1 ? J.n2 - 1 : di);
+    }
   }
   if (g >= ngroups) return;
   const double c_max = __dmul_rn(J.c0, J.t60);
   double th[4], ph[4], dist[4], refl[4];
-  const bool oracle = draw_dist != nullptr;
-  if (oracle) {
+  if (A.draw_dist != nullptr) {  // oracle mode: the reference's own ImageSet rows
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       int i = 4 * g + k + 1;
       size_t o = (size_t)J.img_off + (i <= I ? i : 0);
-      dist[k] = draw_dist[o]; th[k] = draw_az[o]; ph[k] = draw_el[o]; refl[k] = draw_refl[o];
+      dist[k] = A.draw_dist[o]; th[k] = A.draw_az[o]; ph[k] = A.draw_el[o]; refl[k] = A.draw_refl[o];
     }
   } else {
-    // stage-0 stream: theta words [0, I), phi words [I, 2I), u words [2I, 3I)
-    const uint64_t k0[2] = {J.key[0], J.key[1]};
-    const uint64_t k1[2] = {J.key[2], J.key[3]};
+    // stage-0 stream: theta words [0, I), phi words [I, 2I), u words [2I, 3I);
+    // stage-1 stream: perturbation words [0, I).  One Philox block serves 4 images.
     const uint64_t w0 = 4ull * g;
-    u64x4 bt = philox4x64_10((uint64_t)g + 1, 0, 0, 0, k0[0], k0[1]);
+    u64x4 bt = philox4x64_10((uint64_t)g + 1, 0, 0, 0, J.key[0], J.key[1]);
     uint64_t wp = (uint64_t)I + w0, wu = 2ull * I + w0;
-    u64x4 bp0 = philox4x64_10(wp / 4 + 1, 0, 0, 0, k0[0], k0[1]);
+    u64x4 bp0 = philox4x64_10(wp / 4 + 1, 0, 0, 0, J.key[0], J.key[1]);
     u64x4 bp1 = bp0;
-    if (wp & 3) bp1 = philox4x64_10(wp / 4 + 2, 0, 0, 0, k0[0], k0[1]);
-    u64x4 bu0 = philox4x64_10(wu / 4 + 1, 0, 0, 0, k0[0], k0[1]);
+    if (wp & 3) bp1 = philox4x64_10(wp / 4 + 2, 0, 0, 0, J.key[0], J.key[1]);
+    u64x4 bu0 = philox4x64_10(wu / 4 + 1, 0, 0, 0, J.key[0], J.key[1]);
     u64x4 bu1 = bu0;
-    if (wu & 3) bu1 = philox4x64_10(wu / 4 + 2, 0, 0, 0, k0[0], k0[1]);
-    u64x4 bq = philox4x64_10((uint64_t)g + 1, 0, 0, 0, k1[0], k1[1]);
+    if (wu & 3) bu1 = philox4x64_10(wu / 4 + 2, 0, 0, 0, J.key[0], J.key[1]);
+    u64x4 bq = philox4x64_10((uint64_t)g + 1, 0, 0, 0, J.key[2], J.key[3]);
     const double alpha = J.alpha, beta = J.beta;
     const double kres = __ddiv_rn(alpha, __dsub_rn(beta, alpha));
     const double mr1 = __dsub_rn(__ddiv_rn(c_max, J.d0), 1.0);
@@ -133,108 +169,113 @@ __global__ void __launch_bounds__(128) geom_kernel(const frir_job* __restrict__ 
       refl[k] = gg;
     }
   }
+  double px[4], py[4], pz[4];
+  float lg[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    int i = 4 * g + k + 1;
-    if (i > I) break;
-    double x, y, z;
-    image_position(J, dist[k], th[k], ph[k], &x, &y, &z);
-    size_t o = (size_t)J.img_off + i;
-    ws.px[o] = x; ws.py[o] = y; ws.pz[o] = z;
-    ws.lg[o] = pow(J.r, refl[k]);  // core.py:246 r ** g
+    image_position(J, dist[k], th[k], ph[k], &px[k], &py[k], &pz[k]);
+    lg[k] = (float)pow(J.r, refl[k]);  // core.py:246 r ** g (FP32 is enough for the gain)
+  }
+  const int r0 = 4 * g + 1;
+  const int nk = min(4, I - 4 * g);
+  for (int m = 0; m < M; ++m) {
+    int2* out = items + (size_t)m * rows + r0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < nk) {
+        double D;
+        int q = delay_of(px[k], py[k], pz[k], mics + 3 * m, J.c0, A.rate, rate_c0, J.L, &D);
+        out[k] = make_item(q, lg[k] / (float)D, A.r_h, A.t0, A.rh_magic);
+      }
+    }
   }
 }
 
-// ---------------------------------------------------------------- K2 delays + sort
-struct DelayArgs {
+// ---------------------------------------------------------------- K2 bucket sort
+// Stable counting sort of one channel's items by 32-sample output window, in
+// place.  Early flags (core.py:259-264) are set here from the channel's q0.
+// Per-warp 16-bit histograms make the placement stable (row order within a
+// bucket) without atomics deciding the order, so outputs are bit-reproducible.
+struct SortArgs {
   const frir_job* jobs;
   const int32_t* chan_job;
-  const double* mics;
   Workspace ws;
-  int32_t* direct_index;
-  frir_plan_desc d;
-  int end_bit;
+  int r_h, t0, e_lo, e_hi;
 };
 
-__device__ __forceinline__ int ceil_div_i(int a, int b) {  // b > 0, any sign of a
-  return a >= 0 ? (a + b - 1) / b : -((-a) / b);
-}
+constexpr int kSortThreads = 256;
+constexpr int kSortWarps = kSortThreads / 32;
 
-template <int THREADS, int IPT>
-__global__ void __launch_bounds__(THREADS) delay_kernel(DelayArgs A) {
-  using Sort = cub::BlockRadixSort<uint32_t, THREADS, IPT, uint2>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  typename Sort::TempStorage& tmp = *reinterpret_cast<typename Sort::TempStorage*>(smem_raw);
-  __shared__ int s_q0;
-
+__global__ void __launch_bounds__(kSortThreads) sort_kernel(SortArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
   const int c = blockIdx.x;
   const int j = A.chan_job[c];
   const frir_job& J = A.jobs[j];
   const int m = c - J.chan_off;
   const int rows = J.n_images + 1;
-  const double* mic = A.mics + 3 * (size_t)(J.mic_off + m);
-  const double mx = mic[0], my = mic[1], mz = mic[2];
-  const double rate = (double)A.d.r_h * (double)A.d.sample_rate;
-  const int lo = (6 * A.d.r_h * A.d.sample_rate + 999) / 1000;   // core.py:257
-  const int hi = (50 * A.d.r_h * A.d.sample_rate + 999) / 1000;  // core.py:258
-  const int r_h = A.d.r_h, t0 = A.d.t0;
-
-  int q[IPT];
-  float a[IPT];
-#pragma unroll
-  for (int k = 0; k < IPT; ++k) {
-    int r = threadIdx.x * IPT + k;
-    q[k] = 0;
-    a[k] = 0.f;
-    if (r < rows) {
-      size_t o = (size_t)J.img_off + r;
-      // params.py:162-171 distances_to_mics; core.py:242-246
-      double dx = __dsub_rn(A.ws.px[o], mx), dy = __dsub_rn(A.ws.py[o], my),
-             dz = __dsub_rn(A.ws.pz[o], mz);
-      double D = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
-      double qd = ceil(__dmul_rn(__ddiv_rn(D, J.c0), rate));
-      int qi = qd >= (double)(J.L - 1) ? J.L - 1 : (int)qd;
-      q[k] = qi;
-      a[k] = (float)__ddiv_rn(A.ws.lg[o], D);
-      if (r == 0) s_q0 = qi;
-    }
+  const int nbk = ((J.n2 + kExt + kSpBias) >> 5) + 2;  // buckets 0 .. nbk-1
+  int2* items = A.ws.items + J.item_off + (size_t)m * rows;
+  int2* s_val = reinterpret_cast<int2*>(smem);
+  unsigned short* s_cnt = reinterpret_cast<unsigned short*>(s_val + rows);  // [nbk][warps]
+  __shared__ int s_part[kSortThreads];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q0 = A.ws.chan_q0[c];
+  for (int i = tid; i < nbk * kSortWarps; i += kSortThreads) s_cnt[i] = 0;
+  for (int r = tid; r < rows; r += kSortThreads) {
+    int2 v = items[r];
+    const int sp = (v.x & 0xFFFFF) - kSpBias - kExt;
+    const int phi = ((unsigned)v.x >> 20) & 0x3FF;
+    const int rel = A.r_h * sp - A.t0 - phi - q0;  // q - q0
+    if (rel >= -A.e_lo && rel <= A.e_hi) v.y ^= 0x80000000;  // early: negative gain
+    s_val[r] = v;
   }
   __syncthreads();
-  const int q0 = s_q0;
-  if (threadIdx.x == 0) {
-    A.ws.chan_q0[c] = q0;
-    // resample.py:115-119 direct = clip(round(q0 / r_h), 0, n2 - 1), half-even
-    double dv = rint(__ddiv_rn((double)q0, (double)r_h));
-    int di = (int)dv;
-    di = di < 0 ? 0 : (di > J.n2 - 1 ? J.n2 - 1 : di);
-    A.direct_index[c] = di;
+  // per-warp histograms over a contiguous row chunk per warp
+  const int chunk = (rows + kSortWarps - 1) / kSortWarps;
+  const int r_lo = warp * chunk, r_hi = min(rows, r_lo + chunk);
+  for (int r = r_lo + lane; r < r_hi; r += 32) {
+    const int b = (s_val[r].x & 0xFFFFF) >> 5;
+    atomicAdd(reinterpret_cast<unsigned*>(s_cnt) + ((b * kSortWarps + warp) >> 1),
+              1u << (16 * ((b * kSortWarps + warp) & 1)));
   }
-  uint32_t key[IPT];
-  uint2 val[IPT];
-#pragma unroll
-  for (int k = 0; k < IPT; ++k) {
-    int r = threadIdx.x * IPT + k;
-    if (r < rows) {
-      int rel = q[k] - q0;
-      bool early = rel >= -lo && rel <= hi;  // core.py:259-264
-      int s = ceil_div_i(q[k] + t0, r_h);
-      uint32_t spb = (uint32_t)(s + kExt + kSpBias);  // biased output-rate start, >= 0
-      uint32_t off = (uint32_t)(r_h * s - q[k] - t0);  // phase, < r_h <= 1023
-      key[k] = spb >> 5;
-      // early flag rides in the sign of the (positive) gain
-      val[k] = make_uint2(spb | (off << 20), __float_as_uint(early ? -a[k] : a[k]));
-    } else {
-      key[k] = 0xffffffffu;
-      val[k] = make_uint2(0u, 0u);
+  __syncthreads();
+  // exclusive scan over (bucket, warp) in bucket-major order
+  const int n = nbk * kSortWarps;
+  const int per = (n + kSortThreads - 1) / kSortThreads;
+  const int lo = tid * per, hi = min(n, lo + per);
+  int sum = 0;
+  for (int i = lo; i < hi; ++i) sum += s_cnt[i];
+  s_part[tid] = sum;
+  __syncthreads();
+  for (int off = 1; off < kSortThreads; off <<= 1) {
+    int v = tid >= off ? s_part[tid - off] : 0;
+    __syncthreads();
+    s_part[tid] += v;
+    __syncthreads();
+  }
+  int run = s_part[tid] - sum;
+  for (int i = lo; i < hi; ++i) {
+    int cnt = s_cnt[i];
+    s_cnt[i] = (unsigned short)run;
+    run += cnt;
+  }
+  __syncthreads();
+  // stable scatter: warp w walks its chunk in row order
+  for (int base = r_lo; base < r_hi; base += 32) {
+    const int r = base + lane;
+    const bool ok = r < r_hi;
+    int2 v = ok ? s_val[r] : make_int2(0, 0);
+    const int b = ok ? (v.x & 0xFFFFF) >> 5 : -1 - lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, b);
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    unsigned short* slot = s_cnt + (ok ? b * kSortWarps + warp : 0);
+    const int pos = ok ? *slot + rank : 0;
+    __syncwarp();
+    if (ok) {
+      items[pos] = v;
+      if (rank == 0) *slot = (unsigned short)(*slot + __popc(peers));
     }
-  }
-  __syncthreads();  // s_q0 read before TempStorage reuse (distinct storage, kept for clarity)
-  Sort(tmp).SortBlockedToStriped(key, val, 0, A.end_bit);
-  int2* out = A.ws.items + J.item_off + (size_t)m * rows;
-#pragma unroll
-  for (int k = 0; k < IPT; ++k) {
-    int r = k * THREADS + threadIdx.x;
-    if (r < rows) out[r] = make_int2((int)val[k].x, (int)val[k].y);
+    __syncwarp();
   }
 }
 
@@ -334,30 +375,32 @@ struct Channel {
     for (int i = 0; i < NBK; ++i) { dF[i] = dF[i + 1]; wF[i] = wF[i + 1]; dE[i] = dE[i + 1]; wE[i] = wE[i + 1]; }
     dF[NBK] = 0.f; wF[NBK] = 0.f; dE[NBK] = 0.f; wE[NBK] = 0.f;
   }
-  // one item: x = biased start | phase << 20, ae = +-gain (sign = early flag).
-  // Lane L takes taps k0 + 32 j, k0 = (L - start) mod 32, of the item's phase
-  // row; they land in windows j (k0 <= L) or j + 1 (k0 > L).  Selects instead
-  // of branches keep the warp converged; only the early test branches, and
-  // it is warp-uniform.
+  // One staged item: dec = byte offset of (phase row, 32 - start mod 32) in the
+  // doubled table (every 64-entry block holds its 32 taps twice), ae = +-gain
+  // (sign = early flag).  Lane L reads entry L + 32 - delta: tap (L - delta)
+  // mod 32 (+32 j), which lands in window j if L >= delta (bit 8 of the byte
+  // offset set) else in window j + 1.  Predicated FMAs keep the warp converged
+  // with no selects; only the early test branches, and it is warp-uniform.
   template <bool EW>
-  __device__ __forceinline__ void add(int x, float ae, int lane, const float2* __restrict__ s_comp) {
-    const int k0 = (lane - x) & 31;
-    const int idx = ((((unsigned)x >> 20) & 0x3FF) << (5 + (NBK - 1))) | k0;
-    const bool hi = k0 > lane;
+  __device__ __forceinline__ void add(unsigned dec, float ae, unsigned lane8, unsigned comp_sh) {
+    const unsigned addr = dec + lane8;
+    const unsigned lo = addr & 256u;
     const float a = fabsf(ae);
-    const float alo = hi ? 0.f : a, ahi = hi ? a : 0.f;
 #pragma unroll
     for (int j = 0; j < NBK; ++j) {
-      const float2 t = s_comp[idx + 32 * j];
-      dF[j] = fmaf(alo, t.x, dF[j]);
-      wF[j] = fmaf(alo, t.y, wF[j]);
-      dF[j + 1] = fmaf(ahi, t.x, dF[j + 1]);
-      wF[j + 1] = fmaf(ahi, t.y, wF[j + 1]);
+      float tx, ty;
+      asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(tx), "=f"(ty) : "r"(comp_sh + addr + 512u * j));
+      asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %4, 0;\n\t"
+          "@p fma.rn.f32 %0, %5, %6, %0;\n\t@p fma.rn.f32 %1, %5, %7, %1;\n\t"
+          "@!p fma.rn.f32 %2, %5, %6, %2;\n\t@!p fma.rn.f32 %3, %5, %7, %3;\n\t}"
+          : "+f"(dF[j]), "+f"(wF[j]), "+f"(dF[j + 1]), "+f"(wF[j + 1])
+          : "r"(lo), "f"(a), "f"(tx), "f"(ty));
       if (EW && ae < 0.f) {
-        dE[j] = fmaf(alo, t.x, dE[j]);
-        wE[j] = fmaf(alo, t.y, wE[j]);
-        dE[j + 1] = fmaf(ahi, t.x, dE[j + 1]);
-        wE[j + 1] = fmaf(ahi, t.y, wE[j + 1]);
+        asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %4, 0;\n\t"
+            "@p fma.rn.f32 %0, %5, %6, %0;\n\t@p fma.rn.f32 %1, %5, %7, %1;\n\t"
+            "@!p fma.rn.f32 %2, %5, %6, %2;\n\t@!p fma.rn.f32 %3, %5, %7, %3;\n\t}"
+            : "+f"(dE[j]), "+f"(wE[j]), "+f"(dE[j + 1]), "+f"(wE[j + 1])
+            : "r"(lo), "f"(a), "f"(tx), "f"(ty));
       }
     }
   }
@@ -367,7 +410,7 @@ template <bool EARLY, int NBK>
 __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const frir_plan_desc& d = A.plan.d;
-  constexpr int kRow = 32 * NBK;
+  constexpr int kRow = 64 * NBK;  // doubled rows (see Channel::add)
   const int ncomp = d.r_h * kRow;
   float2* s_comp = reinterpret_cast<float2*>(smem);
   double* s_scan = reinterpret_cast<double*>(smem + (size_t)ncomp * 8);
@@ -379,6 +422,8 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
   __syncthreads();
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned comp_sh = (unsigned)__cvta_generic_to_shared(s_comp);
+  const unsigned lane8 = 8u * lane;
   double* bufF = s_warp + (size_t)warp * (EARLY ? 2 : 1) * kWarpBuf;
   double* bufE = bufF + kWarpBuf;
   float* dbF = s_dbuf + (size_t)warp * (EARLY ? 2 : 1) * kTile;
@@ -572,15 +617,18 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
       ch.shift();
       ++w;
     };
+    int2 nxt = lane < rows ? items[lane] : make_int2(0xFFFFF, 0);  // sentinel: last bucket
     for (int p = 0; p < rows; p += 32) {
-      const int pi = p + lane;
-      const int2 mine = pi < rows ? items[pi] : make_int2(0xFFFFF, 0);  // sentinel: last bucket
-      __syncwarp();
-      s_it[lane] = mine;
-      __syncwarp();
+      const int2 mine = nxt;
+      const int pn = p + 32 + lane;
+      nxt = pn < rows ? items[pn] : make_int2(0xFFFFF, 0);  // prefetch the next batch
       const int bk = (mine.x & 0xFFFFF) >> 5;
+      const unsigned dec = (((unsigned)mine.x >> 20) & 0x3FFu) * (512u * NBK) + 8u * (32u - (mine.x & 31));
+      __syncwarp();
+      s_it[lane] = make_int2((int)dec, mine.y);
+      __syncwarp();
       const int cnt = min(32, rows - p);
-      const unsigned emask = EARLY ? __ballot_sync(0xffffffffu, pi < rows && mine.y < 0) : 0u;
+      const unsigned emask = EARLY ? __ballot_sync(0xffffffffu, lane < cnt && mine.y < 0) : 0u;
       int jj = 0;
       while (jj < cnt) {  // runs of equal bucket (items are bucket-sorted)
         const int b = __shfl_sync(0xffffffffu, bk, jj);
@@ -591,13 +639,13 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
 #pragma unroll 2
           for (; jj < end; ++jj) {
             const int2 it = s_it[jj];
-            ch.template add<true>(it.x, __int_as_float(it.y), lane, s_comp);
+            ch.template add<true>((unsigned)it.x, __int_as_float(it.y), lane8, comp_sh);
           }
         } else {
 #pragma unroll 4
           for (; jj < end; ++jj) {
             const int2 it = s_it[jj];
-            ch.template add<false>(it.x, __int_as_float(it.y), lane, s_comp);
+            ch.template add<false>((unsigned)it.x, __int_as_float(it.y), lane8, comp_sh);
           }
         }
       }
@@ -610,16 +658,14 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
 
 // ---------------------------------------------------------------- host launcher
 size_t workspace_bytes(const frir_batch* b) {
-  size_t ni = (size_t)b->total_images;
-  return 4 * align_up(ni * 8) + align_up((size_t)b->total_items * 8) +
-         align_up((size_t)b->total_channels * 4) + 256;
+  return align_up((size_t)b->total_items * 8) + align_up((size_t)b->total_channels * 4) + 256;
 }
 
 static int table_blocks(const frir_plan_desc& d) { return (d.sup + 31) / 32; }
 
 static size_t render_smem(const frir_plan_desc& d, bool early) {
   const int v = early ? 2 : 1;
-  return (size_t)d.r_h * 32 * table_blocks(d) * 8 + kScanDoubles * 8 +
+  return (size_t)d.r_h * 64 * table_blocks(d) * 8 + kScanDoubles * 8 +
          (size_t)kWarps * v * kWarpBuf * 8 + (size_t)kWarps * v * kTile * 4 + (size_t)kWarps * 32 * 8;
 }
 
@@ -638,17 +684,6 @@ static cudaError_t launch_render(const RenderArgs& ra, const frir_plan_desc& d, 
   long want = (channels + kWarps - 1) / kWarps;
   int grid = (int)std::min<long>((long)sms * per_sm, want);
   render_kernel<EARLY, NBK><<<grid, kRenderThreads, smem, st>>>(ra);
-  return cudaGetLastError();
-}
-
-template <int T, int IPT>
-static cudaError_t launch_delay(const DelayArgs& a, int grid, cudaStream_t st) {
-  using Sort = cub::BlockRadixSort<uint32_t, T, IPT, uint2>;
-  size_t smem = sizeof(typename Sort::TempStorage);
-  cudaError_t e = cudaFuncSetAttribute(delay_kernel<T, IPT>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  delay_kernel<T, IPT><<<grid, T, smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -675,29 +710,36 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_
   Workspace ws = carve(wsp, b);
   cudaError_t e = cudaSuccess;
 
-  if (stages & FRIR_STAGE_GEOM) {  // K1
-  int maxg = (b->max_rows - 1 + 3) / 4;
-  dim3 g1(b->n_jobs, (maxg + 127) / 128 > 0 ? (maxg + 127) / 128 : 1);
-  geom_kernel<<<g1, 128, 0, st>>>(b->jobs, b->draw_dist, b->draw_az, b->draw_el, b->draw_refl, ws);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) { set_error(std::string("geom_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
+  const int rate = d.r_h * d.sample_rate;
+  if (stages & FRIR_STAGE_GEOM) {  // K1: draws, geometry, delays, items
+    GeomArgs ga;
+    ga.jobs = b->jobs; ga.mics = b->mics;
+    ga.draw_dist = b->draw_dist; ga.draw_az = b->draw_az; ga.draw_el = b->draw_el; ga.draw_refl = b->draw_refl;
+    ga.ws = ws; ga.direct_index = direct_index;
+    ga.r_h = d.r_h; ga.t0 = d.t0;
+    ga.rh_magic = (unsigned)((0x100000000ull + d.r_h - 1) / d.r_h);
+    ga.rate = (double)rate;
+    int maxg = (b->max_rows - 1 + 3) / 4;
+    dim3 g1(b->n_jobs, maxg > 0 ? (maxg + 127) / 128 : 1);
+    geom_kernel<<<g1, 128, 0, st>>>(ga);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) { set_error(std::string("geom_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
   }
 
-  if (stages & FRIR_STAGE_DELAY) {  // K2
-  DelayArgs da;
-  da.jobs = b->jobs; da.chan_job = b->chan_job; da.mics = b->mics; da.ws = ws;
-  da.direct_index = direct_index; da.d = d;
-  int maxb = b->max_windows + 2;
-  int bits = 1;
-  while ((1 << bits) <= maxb + 1) ++bits;
-  da.end_bit = bits;
-  int rows = b->max_rows, grid = b->total_channels;
-  if (rows <= 1024) e = launch_delay<128, 8>(da, grid, st);
-  else if (rows <= 2048) e = launch_delay<256, 8>(da, grid, st);
-  else if (rows <= 4352) e = launch_delay<256, 17>(da, grid, st);
-  else if (rows <= 8704) e = launch_delay<512, 17>(da, grid, st);
-  else e = launch_delay<1024, 17>(da, grid, st);
-  if (e != cudaSuccess) { set_error(std::string("delay_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
+  if (stages & FRIR_STAGE_DELAY) {  // K2: early flags + stable bucket sort per channel
+    SortArgs sa;
+    sa.jobs = b->jobs; sa.chan_job = b->chan_job; sa.ws = ws;
+    sa.r_h = d.r_h; sa.t0 = d.t0;
+    sa.e_lo = (int)(((long)6 * rate + 999) / 1000);    // core.py:257
+    sa.e_hi = (int)(((long)50 * rate + 999) / 1000);   // core.py:258
+    const int nbk = ((b->max_windows * kWin + kSpBias) >> 5) + 3;
+    size_t smem = (size_t)b->max_rows * 8 + (size_t)nbk * kSortWarps * 2 + 16;
+    e = cudaFuncSetAttribute(sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) {
+      sort_kernel<<<b->total_channels, kSortThreads, smem, st>>>(sa);
+      e = cudaGetLastError();
+    }
+    if (e != cudaSuccess) { set_error(std::string("sort_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
   }
 
   if (stages & FRIR_STAGE_RENDER) {  // K3
