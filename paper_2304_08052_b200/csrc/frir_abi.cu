@@ -39,20 +39,16 @@ static M2 mpow(M2 m, int n) {
 static std::vector<double> scan_constants(double c1, double c2) {
   std::vector<double> s(kScanDoubles, 0.0);
   M2 M{c1, c2, 1.0, 0.0};
-  for (int k = 0; k < 5; ++k) {
-    M2 p = mpow(M, kChunk << k);
-    s[4 * k + 0] = p.a; s[4 * k + 1] = p.b; s[4 * k + 2] = p.c; s[4 * k + 3] = p.d;
+  auto put = [&](int at, const M2& p) { s[at] = p.a; s[at + 1] = p.b; s[at + 2] = p.c; s[at + 3] = p.d; };
+  for (int k = 0; k < 5; ++k) put(kScanKS + 4 * k, mpow(M, kChunk << k));
+  for (int l = 0; l < 32; ++l) put(kScanStart + 4 * l, mpow(M, kChunk * l));
+  M2 p{1, 0, 0, 1};
+  for (int k = 0; k < kTile; ++k) {
+    p = mul(p, M);  // M^(k+1)
+    s[kScanFree + 2 * k] = p.a;
+    s[kScanFree + 2 * k + 1] = p.b;
   }
-  for (int l = 0; l < 32; ++l) {
-    M2 p = mpow(M, kChunk * l);
-    s[20 + 4 * l + 0] = p.a; s[20 + 4 * l + 1] = p.b;
-    s[20 + 4 * l + 2] = p.c; s[20 + 4 * l + 3] = p.d;
-  }
-  for (int k = 0; k < kChunk; ++k) {
-    M2 p = mpow(M, k + 1);
-    s[20 + 128 + 2 * k] = p.a;
-    s[20 + 128 + 2 * k + 1] = p.b;
-  }
+  put(kScanTileM, p);  // M^kTile
   return s;
 }
 
@@ -286,7 +282,8 @@ int frir_jobs_prepare(int32_t sample_rate, frir_job* jobs, int32_t n_jobs, int32
   }
   for (int32_t j = 0; j < n_jobs; ++j) {
     frir_job& J = jobs[j];
-    J.out_stride = padded ? max_n2 : J.n2;
+    // rows start 16-byte aligned (the render kernel stores float4s)
+    J.out_stride = ((padded ? max_n2 : J.n2) + 3) & ~3;
     J.out_off = out;
     out += (int64_t)J.out_stride * J.n_mics;
   }

@@ -11,10 +11,13 @@
 namespace frir {
 
 constexpr int kWin = 32;        // outputs per gather window (one per lane)
-constexpr int kTileWin = 4;     // windows per LP-scan tile
+constexpr int kTileWin = 8;     // windows per LP-scan tile
 constexpr int kTile = kWin * kTileWin;
 constexpr int kChunk = kTile / 32;  // serial outputs per lane in the scan
-constexpr int kExt = 10;        // half2 / r_l: leading LP samples before output 0
+// Output-rate grid offset n'' = n + kExt.  The LP recursion needs W from
+// n = -half2 / r_l = -10 on (zero before that); 32 keeps n'' windows aligned
+// with output windows so the scan can store float4s.
+constexpr int kExt = 32;
 constexpr int kSpBias = 64;     // bias of the packed start index
 constexpr int kMaxRows = 17408; // max images + 1 per job (K2 block sort capacity)
 
@@ -31,7 +34,10 @@ struct DevPlan {
   double lp[6];        // c1, c2, v0
 };
 
-constexpr int kScanDoubles = 4 * 5 + 4 * 32 + 2 * kChunk;  // KS powers, M^(chunk*L), free response
+// LP scan constants: KS powers M^(C 2^s) (5 x 4), M^(C L) (32 x 4), free
+// response row0(M^(k+1)) for k < kTile (kTile x 2), M^kTile (4).
+constexpr int kScanKS = 0, kScanStart = 20, kScanFree = 20 + 128, kScanTileM = kScanFree + 2 * kTile;
+constexpr int kScanDoubles = kScanTileM + 4;
 
 }  // namespace frir
 

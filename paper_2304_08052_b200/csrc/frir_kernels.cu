@@ -293,10 +293,9 @@ struct RenderArgs {
 
 constexpr int kRenderThreads = 256;
 constexpr int kWarps = kRenderThreads / 32;
-constexpr int kPad = kChunk + 1;
-constexpr int kWarpBuf = 32 * kPad;  // doubles per variant per warp
-
-__device__ __forceinline__ int pidx(int o) { return (o / kChunk) * kPad + (o % kChunk); }
+__device__ __forceinline__ int ceil_div_i(int a, int b) {  // b > 0, any sign of a
+  return a >= 0 ? (a + b - 1) / b : -((-a) / b);
+}
 
 struct Cplx {
   double re, im;
@@ -308,51 +307,89 @@ __device__ __forceinline__ Cplx cmul(Cplx a, Cplx b) {
 __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 __device__ __forceinline__ double shfl_up_d(double v, int d) { return __shfl_up_sync(0xffffffffu, v, d); }
 
-// One variant's LP scan over a tile held (as doubles) in buf; on return buf
-// holds LP (FP64) for the tile and (s0, s1) the carried state (LP[last], LP[last-1]).
-__device__ __forceinline__ void lp_scan_tile(double* buf, const double* scan, double c1, double c2,
-                                             double& s0, double& s1, int lane) {
-  double l[kChunk];
-  const int base = lane * kPad;
+// One variant's LP recursion over a tile: lane L owns outputs [C L, C L + C)
+// of the tile (C = kChunk).  W comes from the FP32 tile buffer; the chunk runs
+// serially in FP64 from zero state, chunks are combined with a Kogge-Stone
+// scan of the affine maps s -> M^C s + e, and every output is corrected by the
+// free response of its chunk's true start state.  On return lp[] holds
+// LP[C L + k] and (s0, s1) = (LP[last], LP[last - 1]) of the tile.
+__device__ __forceinline__ void lp_scan_tile(const float* wbuf, const double* scan, double c1,
+                                             double c2, double& s0, double& s1, int lane,
+                                             double (&lp)[kChunk]) {
+  const float4* w4 = reinterpret_cast<const float4*>(wbuf + kChunk * lane);
+  float wv[kChunk];
+#pragma unroll
+  for (int k = 0; k < kChunk / 4; ++k) {
+    float4 v = w4[k];
+    wv[4 * k] = v.x; wv[4 * k + 1] = v.y; wv[4 * k + 2] = v.z; wv[4 * k + 3] = v.w;
+  }
 #pragma unroll
   for (int k = 0; k < kChunk; ++k) {
-    double x = buf[base + k];
-    double p1 = k >= 1 ? l[k - 1] : 0.0, p2 = k >= 2 ? l[k - 2] : 0.0;
-    l[k] = fma(c1, p1, fma(c2, p2, x));
+    double p1 = k >= 1 ? lp[k - 1] : 0.0, p2 = k >= 2 ? lp[k - 2] : 0.0;
+    lp[k] = fma(c1, p1, fma(c2, p2, (double)wv[k]));
   }
-  // affine combine over lanes: E_L = sum_{i<=L} M^{C(L-i)} e_i
-  double e0 = l[kChunk - 1], e1 = l[kChunk - 2];
+  double e0 = lp[kChunk - 1], e1 = lp[kChunk - 2];
 #pragma unroll
   for (int s = 0; s < 5; ++s) {
     const int dd = 1 << s;
     double u0 = shfl_up_d(e0, dd), u1 = shfl_up_d(e1, dd);
     if (lane >= dd) {
-      const double* Mp = scan + 4 * s;
+      const double* Mp = scan + kScanKS + 4 * s;
       e0 = fma(Mp[0], u0, fma(Mp[1], u1, e0));
       e1 = fma(Mp[2], u0, fma(Mp[3], u1, e1));
     }
   }
   double x0 = shfl_up_d(e0, 1), x1 = shfl_up_d(e1, 1);
   if (lane == 0) { x0 = 0.0; x1 = 0.0; }
-  const double* Ms = scan + 20 + 4 * lane;  // M^{C*lane}
-  double t0 = fma(Ms[0], s0, fma(Ms[1], s1, x0));
-  double t1 = fma(Ms[2], s0, fma(Ms[3], s1, x1));
-  const double* fr = scan + 20 + 128;
+  const double* Ms = scan + kScanStart + 4 * lane;  // M^{C lane}
+  const double t0 = fma(Ms[0], s0, fma(Ms[1], s1, x0));
+  const double t1 = fma(Ms[2], s0, fma(Ms[3], s1, x1));
+  const double* fr = scan + kScanFree;
 #pragma unroll
-  for (int k = 0; k < kChunk; ++k) {
-    double v = l[k] + fma(fr[2 * k], t0, fr[2 * k + 1] * t1);
-    l[k] = v;
-    buf[base + k] = v;
-  }
-  s0 = shfl_d(l[kChunk - 1], 31);
-  s1 = shfl_d(l[kChunk - 2], 31);
+  for (int k = 0; k < kChunk; ++k) lp[k] += fma(fr[2 * k], t0, fr[2 * k + 1] * t1);
+  s0 = shfl_d(lp[kChunk - 1], 31);
+  s1 = shfl_d(lp[kChunk - 2], 31);
 }
 
-// Accumulate window w (outputs n' in [32w, 32w + 32), one per lane) from the
-// bucket-sorted items.  Items are staged 32 at a time through per-warp shared
-// memory and read back as broadcasts; each candidate costs one table LDS.64
-// and two (four in early windows) FFMAs per lane.  Returns the new lower item
-// bound for window w + 1.
+// Write the tile's outputs of one variant: y = D - LP - tail correction for
+// outputs n in [n_base + C lane, +C) that lie in [0, n2); float4 stores when
+// the whole chunk is inside (rows are 16-byte aligned, n_base % 32 == 0).
+template <bool HAS_D = true>
+__device__ __forceinline__ void store_chunk(float* out, int n_base, int n2, int nrow, int n_c,
+                                            const float* dbuf, const double* s_corr, int lane,
+                                            const double (&lp)[kChunk]) {
+  const int n0 = n_base + kChunk * lane;
+  const float4* d4 = reinterpret_cast<const float4*>(dbuf + kChunk * lane);
+  float y[kChunk];
+#pragma unroll
+  for (int k = 0; k < kChunk / 4; ++k) {
+    const float4 v = HAS_D ? d4[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+    y[4 * k] = (float)((double)v.x - lp[4 * k]);
+    y[4 * k + 1] = (float)((double)v.y - lp[4 * k + 1]);
+    y[4 * k + 2] = (float)((double)v.z - lp[4 * k + 2]);
+    y[4 * k + 3] = (float)((double)v.w - lp[4 * k + 3]);
+  }
+  if (n0 + kChunk > n_c) {  // tail outputs: subtract the exact truncation correction
+#pragma unroll
+    for (int k = 0; k < kChunk; ++k) {
+      const int n = n0 + k;
+      if (n >= n_c && n < n2)
+        y[k] = (float)((HAS_D ? (double)dbuf[kChunk * lane + k] : 0.0) - lp[k] - s_corr[n - n_c]);
+    }
+  }
+  if (n0 >= 0 && n0 + kChunk <= n2) {
+    float4* o4 = reinterpret_cast<float4*>(out + n0);
+#pragma unroll
+    for (int k = 0; k < kChunk / 4; ++k) o4[k] = make_float4(y[4 * k], y[4 * k + 1], y[4 * k + 2], y[4 * k + 3]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < kChunk; ++k) {  // row tail; the alignment padding gets zeros
+      const int n = n0 + k;
+      if (n >= 0 && n < nrow) out[n] = n < n2 ? y[k] : 0.f;
+    }
+  }
+}
+
 // One warp renders one channel (full + optional early variant) in a single
 // ordered sweep over its bucket-sorted items.  Items of bucket b start in
 // output window b - 2 (n' = s' + k, biased by kSpBias = 64); each is visited
@@ -411,12 +448,13 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const frir_plan_desc& d = A.plan.d;
   constexpr int kRow = 64 * NBK;  // doubled rows (see Channel::add)
+  constexpr int V = EARLY ? 2 : 1;
   const int ncomp = d.r_h * kRow;
   float2* s_comp = reinterpret_cast<float2*>(smem);
   double* s_scan = reinterpret_cast<double*>(smem + (size_t)ncomp * 8);
-  double* s_warp = s_scan + kScanDoubles;  // per warp: W buffers (F[, E])
-  float* s_dbuf = reinterpret_cast<float*>(s_warp + (size_t)kWarps * (EARLY ? 2 : 1) * kWarpBuf);
-  int2* s_items = reinterpret_cast<int2*>(s_dbuf + (size_t)kWarps * (EARLY ? 2 : 1) * kTile);
+  double* s_corr_all = s_scan + kScanDoubles;                              // [warp][V][32]
+  float* s_tile = reinterpret_cast<float*>(s_corr_all + kWarps * V * 32);  // [warp][V][D, W][kTile]
+  int2* s_items = reinterpret_cast<int2*>(s_tile + (size_t)kWarps * V * 2 * kTile);
   for (int i = threadIdx.x; i < ncomp; i += blockDim.x) s_comp[i] = A.plan.comp[i];
   for (int i = threadIdx.x; i < kScanDoubles; i += blockDim.x) s_scan[i] = A.plan.scan[i];
   __syncthreads();
@@ -424,15 +462,18 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned comp_sh = (unsigned)__cvta_generic_to_shared(s_comp);
   const unsigned lane8 = 8u * lane;
-  double* bufF = s_warp + (size_t)warp * (EARLY ? 2 : 1) * kWarpBuf;
-  double* bufE = bufF + kWarpBuf;
-  float* dbF = s_dbuf + (size_t)warp * (EARLY ? 2 : 1) * kTile;
-  float* dbE = dbF + kTile;
+  float* dF_t = s_tile + (size_t)warp * V * 2 * kTile;
+  float* wF_t = dF_t + kTile;
+  float* dE_t = wF_t + kTile;
+  float* wE_t = dE_t + kTile;
+  double* corrF_s = s_corr_all + warp * V * 32;
+  double* corrE_s = corrF_s + 32;
   int2* s_it = s_items + 32 * warp;
   const double c1 = A.plan.lp[0], c2 = A.plan.lp[1];
   const Cplx v0a = {A.plan.lp[2], A.plan.lp[3]}, v0b = {A.plan.lp[4], A.plan.lp[5]};
   const int sup = d.sup, r_h = d.r_h, up = d.up, down = d.down, half1 = d.half1;
-  (void)sup;
+  const int rate = d.r_h * d.sample_rate;
+  const int e_lo = (int)(((long)6 * rate + 999) / 1000), e_hi = (int)(((long)50 * rate + 999) / 1000);
 
   for (;;) {
     int ci = 0;
@@ -445,6 +486,7 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
     const int m = c - J.chan_off;
     const int rows = J.n_images + 1;
     const int n1 = J.n1, n2 = J.n2;
+    const int nrow = min(J.out_stride, (n2 + 3) & ~3);  // row incl. alignment padding
     const int2* items = A.ws.items + J.item_off + (size_t)m * rows;
     float* outF = A.out_full + J.out_off + (size_t)m * J.out_stride;
     float* outE = EARLY ? A.out_early + J.out_off + (size_t)m * J.out_stride : nullptr;
@@ -534,10 +576,10 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
         zE.im += __shfl_xor_sync(0xffffffffu, zE.im, o);
       }
     }
-    // state s = 2 Re(v0 zeta); corrections for outputs n >= n_c
+    // state s = 2 Re(v0 zeta); corrections for outputs n >= n_c (<= 10 of them)
     const int n_c = n1 - d.half2 > 0 ? (n1 - d.half2 + d.r_l - 1) / d.r_l : 0;
-    double corrF = 0.0, corrE = 0.0;
     {
+      double corrF = 0.0, corrE = 0.0;
       Cplx ta = cmul(v0a, zF), tb = cmul(v0b, zF);
       double sF0 = 2.0 * ta.re, sF1 = 2.0 * tb.re;
       double sE0 = 0.0, sE1 = 0.0;
@@ -562,57 +604,74 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
           if (EARLY) corrE += xe * uu;
         }
       }
+      corrF_s[lane] = corrF;
+      if (EARLY) corrE_s[lane] = corrE;
     }
+    // windows touched by early items (q in [q0 - lo, q0 + hi], core.py:257-264)
+    int ew_lo = 0, ew_hi = -1;
+    if (EARLY) {
+      const int q0 = A.ws.chan_q0[c];
+      ew_lo = (ceil_div_i(q0 - e_lo + d.t0, r_h) + kExt) >> 5;
+      ew_hi = (ceil_div_i(q0 + e_hi + d.t0, r_h) + kExt + sup - 1) >> 5;
+    }
+    __syncwarp();
 
-    // ---- ordered sweep: windows w = -2 .. nwin-1 over n' = n + 10
+    // ---- ordered sweep: windows w = -2 .. nwin-1 over n'' = n + kExt
     const int nwin = (n2 + kExt + kWin - 1) / kWin;
     Channel<EARLY, NBK> ch;
     ch.clear();
     double sF0 = 0.0, sF1 = 0.0, sE0 = 0.0, sE1 = 0.0;
-    int w = -2;     // window that the front accumulators (index 0) hold
-    int slot = 0;   // next tile slot
+    bool e_dead = false;  // early state below FP32 resolution: outputs are exact zeros
+    int w = -2;           // window held by the front accumulators
+    int slot = 0;         // next tile slot
+    auto flush = [&]() {
+      const int w0 = w - slot + 1;  // first window of the tile
+      const int n_base = w0 * kWin - kExt;
+      for (int s2 = slot; s2 < kTileWin; ++s2) {  // pad a partial last tile
+        wF_t[s2 * kWin + lane] = 0.f;
+        dF_t[s2 * kWin + lane] = 0.f;
+        if (EARLY) { wE_t[s2 * kWin + lane] = 0.f; dE_t[s2 * kWin + lane] = 0.f; }
+      }
+      __syncwarp();
+      double lp[kChunk];
+      lp_scan_tile(wF_t, s_scan, c1, c2, sF0, sF1, lane, lp);
+      store_chunk(outF, n_base, n2, nrow, n_c, dF_t, corrF_s, lane, lp);
+      if (EARLY) {
+        const bool quiet = w0 > ew_hi;  // no early item feeds this tile: pure decay
+        if (!quiet) {
+          lp_scan_tile(wE_t, s_scan, c1, c2, sE0, sE1, lane, lp);
+          store_chunk(outE, n_base, n2, nrow, n_c, dE_t, corrE_s, lane, lp);
+        } else if (!e_dead) {
+          // LP[k] = row0(M^(k+1)) . s for the whole tile; y = -LP (D = W = 0)
+          const double* fr = s_scan + kScanFree + 2 * kChunk * lane;
+#pragma unroll
+          for (int k = 0; k < kChunk; ++k) lp[k] = fma(fr[2 * k], sE0, fr[2 * k + 1] * sE1);
+          const double* Mt = s_scan + kScanTileM;
+          const double n0v = fma(Mt[0], sE0, Mt[1] * sE1), n1v = fma(Mt[2], sE0, Mt[3] * sE1);
+          sE0 = n0v;
+          sE1 = n1v;
+          store_chunk<false>(outE, n_base, n2, nrow, n_c, dE_t, corrE_s, lane, lp);
+          e_dead = fabs(sE0) + fabs(sE1) < 1e-50;  // |LP| <= ~400 |s| < 2^-150: rounds to 0 in FP32
+        } else {
+          const int n0 = n_base + kChunk * lane;
+#pragma unroll
+          for (int k = 0; k < kChunk; ++k)
+            if (n0 + k >= 0 && n0 + k < nrow) outE[n0 + k] = 0.f;
+        }
+      }
+      __syncwarp();
+      slot = 0;
+    };
     auto emit = [&]() {
       if (w >= 0) {
-        dbF[slot * kWin + lane] = ch.dF[0];
-        bufF[pidx(slot * kWin + lane)] = (double)ch.wF[0];
-        if (EARLY) {
-          dbE[slot * kWin + lane] = ch.dE[0];
-          bufE[pidx(slot * kWin + lane)] = (double)ch.wE[0];
+        dF_t[slot * kWin + lane] = ch.dF[0];
+        wF_t[slot * kWin + lane] = ch.wF[0];
+        if (EARLY && w - slot <= ew_hi) {  // tile not quiet: its early slots are read
+          dE_t[slot * kWin + lane] = ch.dE[0];
+          wE_t[slot * kWin + lane] = ch.wE[0];
         }
         ++slot;
-        if (slot == kTileWin || w == nwin - 1) {
-          for (int s2 = slot; s2 < kTileWin; ++s2) {  // pad a partial last tile
-            bufF[pidx(s2 * kWin + lane)] = 0.0;
-            if (EARLY) bufE[pidx(s2 * kWin + lane)] = 0.0;
-          }
-          __syncwarp();
-          lp_scan_tile(bufF, s_scan, c1, c2, sF0, sF1, lane);
-          if (EARLY) lp_scan_tile(bufE, s_scan, c1, c2, sE0, sE1, lane);
-          __syncwarp();
-          const int w0 = w - slot + 1;
-          for (int wi = 0; wi < slot; ++wi) {
-            const int n = (w0 + wi) * kWin + lane - kExt;
-            const bool tailwin = (w0 + wi) * kWin - kExt + 31 >= n_c;  // warp-uniform
-            double cf = 0.0, ce = 0.0;
-            if (tailwin) {
-              int src = n - n_c;
-              src = src < 0 ? 0 : (src > 31 ? 31 : src);
-              cf = shfl_d(corrF, src);
-              if (EARLY) ce = shfl_d(corrE, src);
-            }
-            if (n >= 0 && n < n2) {
-              const bool fix = n >= n_c;
-              const double yf = (double)dbF[wi * kWin + lane] - bufF[pidx(wi * kWin + lane)] - (fix ? cf : 0.0);
-              outF[n] = (float)yf;
-              if (EARLY) {
-                const double ye = (double)dbE[wi * kWin + lane] - bufE[pidx(wi * kWin + lane)] - (fix ? ce : 0.0);
-                outE[n] = (float)ye;
-              }
-            }
-          }
-          __syncwarp();
-          slot = 0;
-        }
+        if (slot == kTileWin || w == nwin - 1) flush();
       }
       ch.shift();
       ++w;
@@ -665,8 +724,8 @@ static int table_blocks(const frir_plan_desc& d) { return (d.sup + 31) / 32; }
 
 static size_t render_smem(const frir_plan_desc& d, bool early) {
   const int v = early ? 2 : 1;
-  return (size_t)d.r_h * 64 * table_blocks(d) * 8 + kScanDoubles * 8 +
-         (size_t)kWarps * v * kWarpBuf * 8 + (size_t)kWarps * v * kTile * 4 + (size_t)kWarps * 32 * 8;
+  return (size_t)d.r_h * 64 * table_blocks(d) * 8 + kScanDoubles * 8 + (size_t)kWarps * v * 32 * 8 +
+         (size_t)kWarps * v * 2 * kTile * 4 + (size_t)kWarps * 32 * 8;
 }
 
 template <bool EARLY, int NBK>

@@ -134,6 +134,8 @@ def test_jobs_prepare_layout_and_derived():
     assert [int(x) for x in j["key"][0][:2]] == [int(x) for x in ss]
     padded = engine.prepare(16000, jobs, np.zeros((9, 3)), padded=True)
     assert list(padded.jobs["out_stride"]) == [8000] * 3
+    odd = engine.prepare(16000, _one_job(t60=0.30001), MICS)
+    assert odd.jobs["n2"][0] == 4801 and odd.jobs["out_stride"][0] == 4804  # 16-byte aligned rows
 
 
 @pytest.mark.parametrize("kw,msg", [
