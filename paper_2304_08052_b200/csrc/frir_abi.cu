@@ -155,6 +155,8 @@ int frir_plan_create(int32_t fs, frir_plan** out) {
   if (e == cudaSuccess) e = upload(&dv.comp, comp.data(), comp.size());
   if (e == cudaSuccess) e = upload(&dv.h1up, D.h1up.data(), D.h1up.size());
   if (e == cudaSuccess) e = upload(&dv.ppow, D.ppow.data(), D.ppow.size());
+  if (e == cudaSuccess) e = upload(&dv.ppow_lo, D.ppow_lo.data(), D.ppow_lo.size());
+  if (e == cudaSuccess) e = upload(&dv.ppow_hi, D.ppow_hi.data(), D.ppow_hi.size());
   if (e == cudaSuccess) e = upload(&dv.zphase, D.zphase.data(), D.zphase.size());
   if (e == cudaSuccess) e = upload(&dv.kappa, D.kappa.data(), D.kappa.size());
   if (e == cudaSuccess) e = upload(&dv.u, D.u.data(), D.u.size());
@@ -179,6 +181,7 @@ int frir_plan_destroy(frir_plan* p) {
   if (!p) return FRIR_OK;
   DevPlan& dv = p->dev;
   cudaFree(dv.comp); cudaFree(dv.h1up); cudaFree(dv.ppow); cudaFree(dv.zphase);
+  cudaFree(dv.ppow_lo); cudaFree(dv.ppow_hi);
   cudaFree(dv.kappa); cudaFree(dv.u); cudaFree(dv.scan);
   delete p;
   return FRIR_OK;

@@ -239,6 +239,21 @@ bool design(int fs, Design* out, std::string* err) {
       pm *= pole;
     }
   }
+  {  // two-level power table for the render kernel: p^m = hi[m >> 7] * lo[m & 127]
+    const int nhi = d.horizon / 128 + 1;
+    D.ppow_lo.resize(256);
+    D.ppow_hi.resize((size_t)2 * nhi);
+    for (int i = 0; i < 128; ++i) {
+      cplx v = std::pow(pole, i);
+      D.ppow_lo[2 * i] = std::real(v);
+      D.ppow_lo[2 * i + 1] = std::imag(v);
+    }
+    for (int j = 0; j < nhi; ++j) {
+      cplx v = std::pow(pole, 128 * j);
+      D.ppow_hi[2 * j] = std::real(v);
+      D.ppow_hi[2 * j + 1] = std::imag(v);
+    }
+  }
   // Z[rho] = sum_{j>=0} p^j * up*h1[2 half1 - rho - down j]
   D.zphase.assign((size_t)2 * d.down, 0.0);
   for (int ph = 0; ph < d.down; ++ph) {

@@ -24,6 +24,7 @@ struct Design {
   std::vector<double> u;               // [half2]
   std::vector<double> zphase;          // [down][2]
   std::vector<double> ppow;            // [horizon][2]
+  std::vector<double> ppow_lo, ppow_hi; // p^i (i < 128), p^(128 j) (j <= horizon / 128): [][2]
   std::vector<double> lpcoef;          // c1, c2, v0 (re0, im0, re1, im1)
   std::vector<double> h1up;            // up * h1 (stage-1 taps as applied)
 };

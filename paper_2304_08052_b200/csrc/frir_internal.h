@@ -27,6 +27,8 @@ struct DevPlan {
   float2* comp;        // [r_h][sup] (TD, TW), phase-major
   double* h1up;        // [len1]
   double* ppow;        // [horizon][2]
+  double* ppow_lo;     // [128][2]   p^i
+  double* ppow_hi;     // [nhi][2]   p^(128 j), nhi = horizon / 128 + 1
   double* zphase;      // [down][2]
   double* kappa;       // [half2][2]
   double* u;           // [half2]

@@ -455,7 +455,14 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
   double* s_corr_all = s_scan + kScanDoubles;                              // [warp][V][32]
   float* s_tile = reinterpret_cast<float*>(s_corr_all + kWarps * V * 32);  // [warp][V][D, W][kTile]
   int2* s_items = reinterpret_cast<int2*>(s_tile + (size_t)kWarps * V * 2 * kTile);
+  double2* s_plo = reinterpret_cast<double2*>(s_items + 32 * kWarps);  // p^i, i < 128
+  double2* s_zph = s_plo + 128;                                         // Z[rho], rho < down
+  double2* s_phi = s_zph + d.down;                                      // p^(128 j)
+  const int nphi = d.horizon / 128 + 1;
   for (int i = threadIdx.x; i < ncomp; i += blockDim.x) s_comp[i] = A.plan.comp[i];
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) s_plo[i] = make_double2(A.plan.ppow_lo[2 * i], A.plan.ppow_lo[2 * i + 1]);
+  for (int i = threadIdx.x; i < d.down; i += blockDim.x) s_zph[i] = make_double2(A.plan.zphase[2 * i], A.plan.zphase[2 * i + 1]);
+  for (int i = threadIdx.x; i < nphi; i += blockDim.x) s_phi[i] = make_double2(A.plan.ppow_hi[2 * i], A.plan.ppow_hi[2 * i + 1]);
   for (int i = threadIdx.x; i < kScanDoubles; i += blockDim.x) s_scan[i] = A.plan.scan[i];
   __syncthreads();
 
@@ -472,6 +479,7 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
   const double c1 = A.plan.lp[0], c2 = A.plan.lp[1];
   const Cplx v0a = {A.plan.lp[2], A.plan.lp[3]}, v0b = {A.plan.lp[4], A.plan.lp[5]};
   const int sup = d.sup, r_h = d.r_h, up = d.up, down = d.down, half1 = d.half1;
+  const unsigned down_magic = (unsigned)((0x100000000ull + down - 1) / down);  // exact for e < 2^32 / down
   const int rate = d.r_h * d.sample_rate;
   const int e_lo = (int)(((long)6 * rate + 999) / 1000), e_hi = (int)(((long)50 * rate + 999) / 1000);
 
@@ -492,72 +500,83 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
     float* outE = EARLY ? A.out_early + J.out_off + (size_t)m * J.out_stride : nullptr;
 
     // ---- tail: HP state at n1 (modal sum) + taps past n1 (resample.py:107-113 truncation)
+    // Items are bucket-sorted, so the ones within the HP memory horizon of n1
+    // are a suffix of the list; each lane takes one item per step (32 at a time,
+    // next chunk prefetched), FP64 complex accumulation, fixed reduction order.
     Cplx zF = {0.0, 0.0}, zE = {0.0, 0.0};
     double xtF[2] = {0.0, 0.0}, xtE[2] = {0.0, 0.0};
     {
-      const long kthr = (long)n1 - d.horizon;  // need k_hi >= kthr
-      for (int base = rows; base > 0; base -= 32) {
+      const int kthr = n1 - d.horizon;  // need k_hi >= kthr
+      int base = rows;
+      int2 nx = base - 32 + lane >= 0 ? items[base - 32 + lane] : make_int2(0, 0);
+      for (; base > 0; base -= 32) {
         const int r = base - 32 + lane;
-        int q = 0, early = 0, valid = 0;
+        const int2 it = nx;
+        nx = r - 32 >= 0 ? items[r - 32] : make_int2(0, 0);  // prefetch the previous chunk
+        int q = 0, valid = 0, khi = -1, e = 0;
+        bool early = false;
         float a = 0.f;
-        long khi = -1;
         if (r >= 0) {
-          int2 it = items[r];
-          int sp = (it.x & 0xFFFFF) - kSpBias;
-          int phi = ((unsigned)it.x >> 20) & 0x3FF;
-          float ae = __int_as_float(it.y);
+          const int spb = it.x & 0xFFFFF;
+          const int phi = ((unsigned)it.x >> 20) & 0x3FF;
+          const float ae = __int_as_float(it.y);
           early = ae < 0.f;
           a = fabsf(ae);
-          q = r_h * (sp - kExt) - d.t0 - phi;
-          long e = (long)up * q + half1;
-          khi = e >= 0 ? e / down : -((-e + down - 1) / down);
+          q = r_h * (spb - kSpBias - kExt) - d.t0 - phi;
+          e = up * q + half1;  // >= 0
+          khi = (int)__umulhi((unsigned)e, down_magic);
           valid = khi >= kthr;
-          // bound for "everything below is past the horizon": max q of this bucket
-          int bucket = (sp > 0 ? sp : 0) >> 5;
-          long qmax = (long)r_h * (32L * bucket + 31 - kExt) - d.t0;
-          long kmax = ((long)up * qmax + half1) / down;
-          if (kmax >= kthr) valid |= 2;
+          // every item of this bucket or below has q <= qmax: stop when past the horizon
+          const int qmax = r_h * ((spb | 31) - kSpBias - kExt) - d.t0;
+          if ((int)__umulhi((unsigned)(up * qmax + half1), down_magic) >= kthr) valid |= 2;
         }
-        if (valid & 1) {
-          long e = (long)up * q + half1;
-          if (khi < n1) {
-            int rho = (int)(e - (long)down * khi);
-            long mm = (long)n1 - 1 - khi;
-            Cplx pm = {A.plan.ppow[2 * mm], A.plan.ppow[2 * mm + 1]};
-            Cplx zr = {A.plan.zphase[2 * rho], A.plan.zphase[2 * rho + 1]};
-            Cplx t = cmul(pm, zr);
-            zF.re += a * t.re; zF.im += a * t.im;
-            if (EARLY && early) { zE.re += a * t.re; zE.im += a * t.im; }
-          } else {
-            long klo = (long)up * q - half1;
-            klo = klo >= 0 ? (klo + down - 1) / down : -((-klo) / down);
-            for (long k = klo; k < n1; ++k) {
-              long mm = (long)n1 - 1 - k;
-              if (mm >= d.horizon) continue;
-              double cc = (double)a * A.plan.h1up[(long)down * k + half1 - (long)up * q];
-              double pr = A.plan.ppow[2 * mm], pi = A.plan.ppow[2 * mm + 1];
-              zF.re += cc * pr; zF.im += cc * pi;
-              if (EARLY && early) { zE.re += cc * pr; zE.im += cc * pi; }
-            }
+        if ((valid & 1) && khi < n1) {
+          const int rho = e - down * khi;
+          const int mm = n1 - 1 - khi;
+          const double2 lo = s_plo[mm & 127], hi = s_phi[mm >> 7], zr = s_zph[rho];
+          const Cplx pm = cmul({hi.x, hi.y}, {lo.x, lo.y});
+          const Cplx t = cmul(pm, {zr.x, zr.y});
+          zF.re = fma((double)a, t.re, zF.re);
+          zF.im = fma((double)a, t.im, zF.im);
+          if (EARLY && early) {
+            zE.re = fma((double)a, t.re, zE.re);
+            zE.im = fma((double)a, t.im, zE.im);
           }
         }
-        // taps past n1, one straddler at a time (deterministic lane order)
+        // straddlers (taps on both sides of n1): one at a time in lane order
         unsigned strad = __ballot_sync(0xffffffffu, (valid & 1) && khi >= n1);
         while (strad) {
-          int src = __ffs(strad) - 1;
+          const int src = __ffs(strad) - 1;
           strad &= strad - 1;
-          int qs = __shfl_sync(0xffffffffu, q, src);
-          float as = __shfl_sync(0xffffffffu, a, src);
-          int es = __shfl_sync(0xffffffffu, early, src);
-          long khs = (long)((long)up * qs + half1) / down;
+          const int qs = __shfl_sync(0xffffffffu, q, src);
+          const float as = __shfl_sync(0xffffffffu, a, src);
+          const bool es = __shfl_sync(0xffffffffu, (int)early, src) != 0;
+          const int khs = (int)__umulhi((unsigned)(up * qs + half1), down_magic);
+          const int xs = up * qs - half1 + 1024 * down;  // >= 0 (half1 = 10 r_h <= 1024 down)
+          const int klo = (int)__umulhi((unsigned)xs, down_magic) - 1024 + (xs % down != 0);
+          // taps k < n1 feed the state (strided over lanes, then reduced with the rest)
+          for (int k = klo + lane; k < n1; k += 32) {
+            const int mm = n1 - 1 - k;
+            if (mm >= d.horizon) continue;
+            const double cc = (double)as * A.plan.h1up[down * k + half1 - up * qs];
+            const double2 lo = s_plo[mm & 127], hi = s_phi[mm >> 7];
+            const Cplx pm = cmul({hi.x, hi.y}, {lo.x, lo.y});
+            zF.re = fma(cc, pm.re, zF.re);
+            zF.im = fma(cc, pm.im, zF.im);
+            if (EARLY && es) {
+              zE.re = fma(cc, pm.re, zE.re);
+              zE.im = fma(cc, pm.im, zE.im);
+            }
+          }
+          // taps k >= n1: input past the truncation point
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            int l = lane + 32 * h;
-            long k = (long)n1 + l;
+            const int l = lane + 32 * h;
+            const int k = n1 + l;
             if (l < d.lt_max && k <= khs) {
-              long idx = (long)down * k + half1 - (long)up * qs;
+              const int idx = down * k + half1 - up * qs;
               if (idx >= 0 && idx < d.len1) {
-                double cc = (double)as * A.plan.h1up[idx];
+                const double cc = (double)as * A.plan.h1up[idx];
                 xtF[h] += cc;
                 if (EARLY && es) xtE[h] += cc;
               }
@@ -725,7 +744,8 @@ static int table_blocks(const frir_plan_desc& d) { return (d.sup + 31) / 32; }
 static size_t render_smem(const frir_plan_desc& d, bool early) {
   const int v = early ? 2 : 1;
   return (size_t)d.r_h * 64 * table_blocks(d) * 8 + kScanDoubles * 8 + (size_t)kWarps * v * 32 * 8 +
-         (size_t)kWarps * v * 2 * kTile * 4 + (size_t)kWarps * 32 * 8;
+         (size_t)kWarps * v * 2 * kTile * 4 + (size_t)kWarps * 32 * 8 +
+         (size_t)(128 + d.down + d.horizon / 128 + 1) * 16;
 }
 
 template <bool EARLY, int NBK>
