@@ -11,7 +11,7 @@
 namespace frir {
 
 constexpr int kWin = 32;        // outputs per gather window (one per lane)
-constexpr int kTileWin = 8;     // windows per LP-scan tile
+constexpr int kTileWin = 4;     // windows per LP-scan tile
 constexpr int kTile = kWin * kTileWin;
 constexpr int kChunk = kTile / 32;  // serial outputs per lane in the scan
 // Output-rate grid offset n'' = n + kExt.  The LP recursion needs W from
@@ -40,6 +40,7 @@ struct DevPlan {
 // response row0(M^(k+1)) for k < kTile (kTile x 2), M^kTile (4).
 constexpr int kScanKS = 0, kScanStart = 20, kScanFree = 20 + 128, kScanTileM = kScanFree + 2 * kTile;
 constexpr int kScanDoubles = kScanTileM + 4;
+constexpr int kScanSmem = kScanFree + 2 * kChunk;  // part the render kernel keeps in smem
 
 }  // namespace frir
 

@@ -444,7 +444,7 @@ struct Channel {
 };
 
 template <bool EARLY, int NBK>
-__global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
+__global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const frir_plan_desc& d = A.plan.d;
   constexpr int kRow = 64 * NBK;  // doubled rows (see Channel::add)
@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
   const int ncomp = d.r_h * kRow;
   float2* s_comp = reinterpret_cast<float2*>(smem);
   double* s_scan = reinterpret_cast<double*>(smem + (size_t)ncomp * 8);
-  double* s_corr_all = s_scan + kScanDoubles;                              // [warp][V][32]
+  double* s_corr_all = s_scan + kScanSmem;                                 // [warp][V][32]
   float* s_tile = reinterpret_cast<float*>(s_corr_all + kWarps * V * 32);  // [warp][V][D, W][kTile]
   int2* s_items = reinterpret_cast<int2*>(s_tile + (size_t)kWarps * V * 2 * kTile);
   double2* s_plo = reinterpret_cast<double2*>(s_items + 32 * kWarps);  // p^i, i < 128
@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
   for (int i = threadIdx.x; i < 128; i += blockDim.x) s_plo[i] = make_double2(A.plan.ppow_lo[2 * i], A.plan.ppow_lo[2 * i + 1]);
   for (int i = threadIdx.x; i < d.down; i += blockDim.x) s_zph[i] = make_double2(A.plan.zphase[2 * i], A.plan.zphase[2 * i + 1]);
   for (int i = threadIdx.x; i < nphi; i += blockDim.x) s_phi[i] = make_double2(A.plan.ppow_hi[2 * i], A.plan.ppow_hi[2 * i + 1]);
-  for (int i = threadIdx.x; i < kScanDoubles; i += blockDim.x) s_scan[i] = A.plan.scan[i];
+  for (int i = threadIdx.x; i < kScanSmem; i += blockDim.x) s_scan[i] = A.plan.scan[i];
   __syncthreads();
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -662,10 +662,10 @@ __global__ void __launch_bounds__(kRenderThreads) render_kernel(RenderArgs A) {
           store_chunk(outE, n_base, n2, nrow, n_c, dE_t, corrE_s, lane, lp);
         } else if (!e_dead) {
           // LP[k] = row0(M^(k+1)) . s for the whole tile; y = -LP (D = W = 0)
-          const double* fr = s_scan + kScanFree + 2 * kChunk * lane;
+          const double* fr = A.plan.scan + kScanFree + 2 * kChunk * lane;  // global (L1)
 #pragma unroll
           for (int k = 0; k < kChunk; ++k) lp[k] = fma(fr[2 * k], sE0, fr[2 * k + 1] * sE1);
-          const double* Mt = s_scan + kScanTileM;
+          const double* Mt = A.plan.scan + kScanTileM;
           const double n0v = fma(Mt[0], sE0, Mt[1] * sE1), n1v = fma(Mt[2], sE0, Mt[3] * sE1);
           sE0 = n0v;
           sE1 = n1v;
@@ -743,7 +743,7 @@ static int table_blocks(const frir_plan_desc& d) { return (d.sup + 31) / 32; }
 
 static size_t render_smem(const frir_plan_desc& d, bool early) {
   const int v = early ? 2 : 1;
-  return (size_t)d.r_h * 64 * table_blocks(d) * 8 + kScanDoubles * 8 + (size_t)kWarps * v * 32 * 8 +
+  return (size_t)d.r_h * 64 * table_blocks(d) * 8 + kScanSmem * 8 + (size_t)kWarps * v * 32 * 8 +
          (size_t)kWarps * v * 2 * kTile * 4 + (size_t)kWarps * 32 * 8 +
          (size_t)(128 + d.down + d.horizon / 128 + 1) * 16;
 }
