@@ -105,6 +105,7 @@ typedef struct {
   double r;                  /* reflection coefficient, core.py:113-128 */
   double rr_max;             /* max_reflections, core.py:186-192 (0 when I == 0) */
   double alpha3, b3a3;       /* alpha**3 and beta**3 - alpha**3 (core.py:100) */
+  double log2r;              /* log2(r): gains r**g are evaluated as exp2(g log2 r) in FP32 */
   uint64_t key[4];          /* Philox keys of streams (seed, k, 0) and (seed, k, 1) */
 } frir_job;
 

@@ -49,6 +49,7 @@ class FrirJob(ctypes.Structure):
         ("chan_off", c_int32), ("out_stride", c_int32), ("L", c_int32), ("n1", c_int32),
         ("n2", c_int32), ("pad_", c_int32),
         ("r", c_double), ("rr_max", c_double), ("alpha3", c_double), ("b3a3", c_double),
+        ("log2r", c_double),
         ("key", c_uint64 * 4),
     ]
 

@@ -247,6 +247,7 @@ int frir_jobs_prepare(int32_t sample_rate, frir_job* jobs, int32_t n_jobs, int32
         return FRIR_EINVAL;
       }
     }
+    J.log2r = std::log2(J.r);
     J.alpha3 = std::pow(J.alpha, 3.0);
     J.b3a3 = std::pow(J.beta, 3.0) - J.alpha3;
     uint64_t key[2];

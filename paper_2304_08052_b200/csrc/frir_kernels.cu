@@ -162,8 +162,9 @@ __global__ void __launch_bounds__(128) geom_kernel(GeomArgs A) {
       // core.py:215-220 reflection counts (stage-1 stream)
       double pr = __dadd_rn(J.perturb_lo, __dmul_rn(prange, u64_to_unit(bq.v[k])));
       double qq = __ddiv_rn(dd, c_max);
-      double gg = __dadd_rn(__dadd_rn(1.0, __dmul_rn(__dmul_rn(qq, qq), rrm1)),
-                            __dmul_rn(pr, pow(dr, J.tau)));
+      // dr**tau only shapes the gain exponent: FP32 (rel. err ~1e-7 -> gain ~1e-9)
+      const double drt = (double)exp2f((float)J.tau * log2f((float)dr));
+      double gg = __dadd_rn(__dadd_rn(1.0, __dmul_rn(__dmul_rn(qq, qq), rrm1)), __dmul_rn(pr, drt));
       gg = fmin(fmax(gg, 1.0), J.rr_max);
       dist[k] = dd;
       refl[k] = gg;
@@ -174,7 +175,9 @@ __global__ void __launch_bounds__(128) geom_kernel(GeomArgs A) {
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     image_position(J, dist[k], th[k], ph[k], &px[k], &py[k], &pz[k]);
-    lg[k] = (float)pow(J.r, refl[k]);  // core.py:246 r ** g (FP32 is enough for the gain)
+    // core.py:246 r ** g; the gain is an FP32 quantity (exp2 of an FP64 exponent)
+    const double x = refl[k] * J.log2r, xi = floor(x);
+    lg[k] = ldexpf(exp2f((float)(x - xi)), (int)xi);
   }
   const int r0 = 4 * g + 1;
   const int nk = min(4, I - 4 * g);
