@@ -50,7 +50,8 @@ enum {
   FRIR_TAB_U = 6,         /* tail-correction input response (h2 * HP impulse), [half2] */
   FRIR_TAB_ZPHASE = 7,    /* per-phase modal tap sums, [down][2] (re, im) */
   FRIR_TAB_PPOW = 8,      /* p^m, m < horizon, [horizon][2] (re, im) */
-  FRIR_TAB_LPCOEF = 9     /* [c1, c2, v0 (4 doubles: re0 im0 re1 im1)] */
+  FRIR_TAB_LPCOEF = 9,    /* [c1, c2, v0 (4 doubles: re0 im0 re1 im1)] */
+  FRIR_TAB_GW = 10        /* low-pass-branch filter h2 * N * B' (head correction) */
 };
 
 typedef struct frir_plan frir_plan;

@@ -18,7 +18,7 @@ LIB_PATH = Path(__file__).resolve().parent / "lib" / "libfrir.so"
 FRIR_OK, FRIR_EINVAL, FRIR_ECUDA, FRIR_ERANGE, FRIR_ENOMEM = 0, -1, -2, -3, -4
 STAGE_GEOM, STAGE_DELAY, STAGE_RENDER, STAGE_ALL = 1, 2, 4, 7
 TAB_H1, TAB_H2, TAB_SOS, TAB_COMP_D, TAB_COMP_W = 0, 1, 2, 3, 4
-TAB_KAPPA, TAB_U, TAB_ZPHASE, TAB_PPOW, TAB_LPCOEF = 5, 6, 7, 8, 9
+TAB_KAPPA, TAB_U, TAB_ZPHASE, TAB_PPOW, TAB_LPCOEF, TAB_GW = 5, 6, 7, 8, 9, 10
 
 c_int32, c_int64, c_uint64, c_double = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
 c_void_p = ctypes.c_void_p

@@ -102,6 +102,7 @@ int frir_design_table(int32_t fs, int32_t which, double* out, int64_t cap, int64
     case FRIR_TAB_ZPHASE: v = D.zphase; break;
     case FRIR_TAB_PPOW: v = D.ppow; break;
     case FRIR_TAB_LPCOEF: v = D.lpcoef; break;
+    case FRIR_TAB_GW: v = D.gw; break;
     default: set_error("unknown table id"); return FRIR_EINVAL;
   }
   if (n_out) *n_out = (int64_t)v.size();
@@ -154,6 +155,8 @@ int frir_plan_create(int32_t fs, frir_plan** out) {
   cudaError_t e = cudaSuccess;
   if (e == cudaSuccess) e = upload(&dv.comp, comp.data(), comp.size());
   if (e == cudaSuccess) e = upload(&dv.h1up, D.h1up.data(), D.h1up.size());
+  if (e == cudaSuccess) e = upload(&dv.h2, D.h2.data(), D.h2.size());
+  if (e == cudaSuccess) e = upload(&dv.gw, D.gw.data(), D.gw.size());
   if (e == cudaSuccess) e = upload(&dv.ppow, D.ppow.data(), D.ppow.size());
   if (e == cudaSuccess) e = upload(&dv.ppow_lo, D.ppow_lo.data(), D.ppow_lo.size());
   if (e == cudaSuccess) e = upload(&dv.ppow_hi, D.ppow_hi.data(), D.ppow_hi.size());
@@ -181,7 +184,7 @@ int frir_plan_destroy(frir_plan* p) {
   if (!p) return FRIR_OK;
   DevPlan& dv = p->dev;
   cudaFree(dv.comp); cudaFree(dv.h1up); cudaFree(dv.ppow); cudaFree(dv.zphase);
-  cudaFree(dv.ppow_lo); cudaFree(dv.ppow_hi);
+  cudaFree(dv.ppow_lo); cudaFree(dv.ppow_hi); cudaFree(dv.h2); cudaFree(dv.gw);
   cudaFree(dv.kappa); cudaFree(dv.u); cudaFree(dv.scan);
   delete p;
   return FRIR_OK;

@@ -177,6 +177,7 @@ bool design(int fs, Design* out, std::string* err) {
   d.c1 = 2.0 * std::real(P);
   d.c2 = -std::norm(P);
   std::vector<double> gfilt = convolve(convolve(D.h2, nlp), bpr);
+  D.gw = gfilt;
 
   // Composite tables T(t) = up * sum_k h1[down k + half1 + up t] * F[half2 - k].
   auto composite = [&](const std::vector<double>& filt, int tmin, int tmax) {

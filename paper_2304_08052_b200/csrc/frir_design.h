@@ -27,6 +27,7 @@ struct Design {
   std::vector<double> ppow_lo, ppow_hi; // p^i (i < 128), p^(128 j) (j <= horizon / 128): [][2]
   std::vector<double> lpcoef;          // c1, c2, v0 (re0, im0, re1, im1)
   std::vector<double> h1up;            // up * h1 (stage-1 taps as applied)
+  std::vector<double> gw;              // h2 * N * B' (low-pass branch filter, len2 + 2 r_l)
 };
 
 // Returns false and sets *err on an invalid sample rate (rate_factors rules).

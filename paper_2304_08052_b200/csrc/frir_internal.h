@@ -26,6 +26,8 @@ struct DevPlan {
   frir_plan_desc d;
   float2* comp;        // [r_h][sup] (TD, TW), phase-major
   double* h1up;        // [len1]
+  double* h2;          // [len2]
+  double* gw;          // [len2 + 2 r_l]
   double* ppow;        // [horizon][2]
   double* ppow_lo;     // [128][2]   p^i
   double* ppow_hi;     // [nhi][2]   p^(128 j), nhi = horizon / 128 + 1

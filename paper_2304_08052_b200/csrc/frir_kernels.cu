@@ -458,7 +458,8 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A)
   double* s_corr_all = s_scan + kScanSmem;                                 // [warp][V][32]
   float* s_tile = reinterpret_cast<float*>(s_corr_all + kWarps * V * 32);  // [warp][V][D, W][kTile]
   int2* s_items = reinterpret_cast<int2*>(s_tile + (size_t)kWarps * V * 2 * kTile);
-  double2* s_plo = reinterpret_cast<double2*>(s_items + 32 * kWarps);  // p^i, i < 128
+  float* s_head = reinterpret_cast<float*>(s_items + 32 * kWarps);        // [warp][V][D, W][64]
+  double2* s_plo = reinterpret_cast<double2*>(s_head + kWarps * V * 2 * 64);  // p^i, i < 128
   double2* s_zph = s_plo + 128;                                         // Z[rho], rho < down
   double2* s_phi = s_zph + d.down;                                      // p^(128 j)
   const int nphi = d.horizon / 128 + 1;
@@ -479,6 +480,7 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A)
   double* corrF_s = s_corr_all + warp * V * 32;
   double* corrE_s = corrF_s + 32;
   int2* s_it = s_items + 32 * warp;
+  float* head_s = s_head + warp * V * 2 * 64;
   const double c1 = A.plan.lp[0], c2 = A.plan.lp[1];
   const Cplx v0a = {A.plan.lp[2], A.plan.lp[3]}, v0b = {A.plan.lp[4], A.plan.lp[5]};
   const int sup = d.sup, r_h = d.r_h, up = d.up, down = d.down, half1 = d.half1;
@@ -533,7 +535,8 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A)
           const int qmax = r_h * ((spb | 31) - kSpBias - kExt) - d.t0;
           if ((int)__umulhi((unsigned)(up * qmax + half1), down_magic) >= kthr) valid |= 2;
         }
-        if ((valid & 1) && khi < n1) {
+        const bool head_item = (valid & 1) && e < 2 * half1;  // some stage-1 taps at k < 0
+        if ((valid & 1) && khi < n1 && !head_item) {
           const int rho = e - down * khi;
           const int mm = n1 - 1 - khi;
           const double2 lo = s_plo[mm & 127], hi = s_phi[mm >> 7], zr = s_zph[rho];
@@ -546,8 +549,9 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A)
             zE.im = fma((double)a, t.im, zE.im);
           }
         }
-        // straddlers (taps on both sides of n1): one at a time in lane order
-        unsigned strad = __ballot_sync(0xffffffffu, (valid & 1) && khi >= n1);
+        // straddlers (taps on both sides of n1) and head items (taps before 0):
+        // one at a time in lane order, explicit taps
+        unsigned strad = __ballot_sync(0xffffffffu, (valid & 1) && (khi >= n1 || head_item));
         while (strad) {
           const int src = __ffs(strad) - 1;
           strad &= strad - 1;
@@ -556,9 +560,10 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A)
           const bool es = __shfl_sync(0xffffffffu, (int)early, src) != 0;
           const int khs = (int)__umulhi((unsigned)(up * qs + half1), down_magic);
           const int xs = up * qs - half1 + 1024 * down;  // >= 0 (half1 = 10 r_h <= 1024 down)
-          const int klo = (int)__umulhi((unsigned)xs, down_magic) - 1024 + (xs % down != 0);
-          // taps k < n1 feed the state (strided over lanes, then reduced with the rest)
-          for (int k = klo + lane; k < n1; k += 32) {
+          const int klo = max(0, (int)__umulhi((unsigned)xs, down_magic) - 1024 + (xs % down != 0));
+          // taps 0 <= k <= min(k_hi, n1 - 1) feed the state (strided over lanes)
+          const int kend = min(khs + 1, n1);
+          for (int k = klo + lane; k < kend; k += 32) {
             const int mm = n1 - 1 - k;
             if (mm >= d.horizon) continue;
             const double cc = (double)as * A.plan.h1up[down * k + half1 - up * qs];
@@ -642,6 +647,7 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A)
     const int nwin = (n2 + kExt + kWin - 1) / kWin;
     Channel<EARLY, NBK> ch;
     ch.clear();
+    bool head_on = false;  // head corrections pending in head_s
     double sF0 = 0.0, sF1 = 0.0, sE0 = 0.0, sE1 = 0.0;
     bool e_dead = false;  // early state below FP32 resolution: outputs are exact zeros
     int w = -2;           // window held by the front accumulators
@@ -686,6 +692,14 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A)
     };
     auto emit = [&]() {
       if (w >= 0) {
+        if (head_on && w < 2) {  // warp-uniform, at most twice per channel
+          ch.dF[0] += head_s[32 * w + lane];
+          ch.wF[0] += head_s[64 + 32 * w + lane];
+          if (EARLY) {
+            ch.dE[0] += head_s[128 + 32 * w + lane];
+            ch.wE[0] += head_s[192 + 32 * w + lane];
+          }
+        }
         dF_t[slot * kWin + lane] = ch.dF[0];
         wF_t[slot * kWin + lane] = ch.wF[0];
         if (EARLY && w - slot <= ew_hi) {  // tile not quiet: its early slots are read
@@ -709,6 +723,44 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A)
       s_it[lane] = make_int2((int)dec, mine.y);
       __syncwarp();
       const int cnt = min(32, rows - p);
+      {  // head: stage-1 taps at mid index < 0 do not exist in the reference (resample.py:107)
+        const int qm = r_h * ((mine.x & 0xFFFFF) - kSpBias - kExt) - d.t0 - (((unsigned)mine.x >> 20) & 0x3FF);
+        unsigned hm = __ballot_sync(0xffffffffu, lane < cnt && up * qm < half1);
+        if (hm) {
+          if (!head_on) {
+            for (int i = lane; i < V * 2 * 64; i += 32) head_s[i] = 0.f;
+            head_on = true;
+          }
+          while (hm) {
+            const int src = __ffs(hm) - 1;
+            hm &= hm - 1;
+            const int qs = __shfl_sync(0xffffffffu, qm, src);
+            const float aes = __int_as_float(__shfl_sync(0xffffffffu, mine.y, src));
+            const double as = fabs((double)aes);
+            const int xs = up * qs - half1 + 1024 * down;
+            const int klo = (int)__umulhi((unsigned)xs, down_magic) - 1024 + (xs % down != 0);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int np = lane + 32 * h;  // n'' in [0, 64)
+              const int n = np - kExt;
+              double cd = 0.0, cw = 0.0;
+              for (int k = klo; k < 0; ++k) {
+                const double cc = as * A.plan.h1up[down * k + half1 - up * qs];
+                const int idx = d.r_l * n + d.half2 - k;
+                if (idx >= 0 && idx < d.len2) cd += cc * A.plan.h2[idx];
+                if (idx >= 0 && idx < d.len2 + 2 * d.r_l) cw += cc * A.plan.gw[idx];
+              }
+              head_s[np] -= (float)cd;
+              head_s[64 + np] -= (float)cw;
+              if (EARLY && aes < 0.f) {
+                head_s[128 + np] -= (float)cd;
+                head_s[192 + np] -= (float)cw;
+              }
+            }
+          }
+          __syncwarp();
+        }
+      }
       const unsigned emask = EARLY ? __ballot_sync(0xffffffffu, lane < cnt && mine.y < 0) : 0u;
       int jj = 0;
       while (jj < cnt) {  // runs of equal bucket (items are bucket-sorted)
@@ -748,7 +800,7 @@ static size_t render_smem(const frir_plan_desc& d, bool early) {
   const int v = early ? 2 : 1;
   return (size_t)d.r_h * 64 * table_blocks(d) * 8 + kScanSmem * 8 + (size_t)kWarps * v * 32 * 8 +
          (size_t)kWarps * v * 2 * kTile * 4 + (size_t)kWarps * 32 * 8 +
-         (size_t)(128 + d.down + d.horizon / 128 + 1) * 16;
+         (size_t)kWarps * v * 2 * 64 * 4 + (size_t)(128 + d.down + d.horizon / 128 + 1) * 16;
 }
 
 template <bool EARLY, int NBK>

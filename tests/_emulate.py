@@ -30,6 +30,8 @@ class Tables:
         self.c1, self.c2 = lp[0], lp[1]
         self.v0 = np.array([lp[2] + 1j * lp[3], lp[4] + 1j * lp[5]])
         self.h1up = g(_abi.TAB_H1) * self.d.up
+        self.h2 = g(_abi.TAB_H2)
+        self.gw = g(_abi.TAB_GW)
 
 
 def render_channel(tab: Tables, q: np.ndarray, a: np.ndarray, L: int) -> np.ndarray:
@@ -50,6 +52,19 @@ def render_channel(tab: Tables, q: np.ndarray, a: np.ndarray, L: int) -> np.ndar
         t = phi + r_h * k
         np.add.at(D, idx[ok], a[ok] * tab.comp_d[t[ok]])
         np.add.at(W, idx[ok], a[ok] * tab.comp_w[t[ok]])
+    # head: stage-1 taps at mid index k < 0 do not exist in the reference
+    for qi, ai in zip(q, a):
+        if up * qi >= d.half1:
+            continue
+        klo = -((-(up * qi - d.half1)) // down)
+        for k in range(klo, 0):
+            c = ai * tab.h1up[down * k + d.half1 - up * qi]
+            for n in range(-EXT, n2):
+                idx = r_l * n + d.half2 - k
+                if 0 <= idx < len(tab.h2) and n >= 0:
+                    D[n + EXT] -= c * tab.h2[idx]
+                if 0 <= idx < len(tab.gw):
+                    W[n + EXT] -= c * tab.gw[idx]
     LP = np.zeros(n2 + EXT)
     p1 = p2 = 0.0
     for n in range(n2 + EXT):
@@ -64,10 +79,10 @@ def render_channel(tab: Tables, q: np.ndarray, a: np.ndarray, L: int) -> np.ndar
     for qi, ai, kh, ei in zip(q, a, khi, e):
         if kh < n1 - d.horizon:
             continue
-        if kh < n1:
+        if kh < n1 and up * qi >= d.half1:
             zeta += ai * tab.ppow[n1 - 1 - kh] * tab.zphase[ei - down * kh]
             continue
-        klo = -((-(up * qi - d.half1)) // down)
+        klo = max(0, -((-(up * qi - d.half1)) // down))
         for k in range(klo, kh + 1):
             c = ai * tab.h1up[down * k + d.half1 - up * qi]
             if k < n1:

@@ -71,7 +71,7 @@ def test_cfg1_matches_reference(golden, mode):
 
 
 @pytest.mark.parametrize("mode", ["native", "oracle"])
-@pytest.mark.parametrize("ci", range(8))
+@pytest.mark.parametrize("ci", range(11))
 def test_golden_cases(golden, ci, mode):
     m, jobs, mics = job_from_case(golden, ci)
     pre = f"c{ci}_"

@@ -73,7 +73,7 @@ def test_cfg1_draws_match_reference(golden):
     assert np.array_equal(d.mic_distances, g["mic_distances"])
 
 
-@pytest.mark.parametrize("ci", range(8))
+@pytest.mark.parametrize("ci", range(11))
 def test_cases_match_reference(golden, ci):
     job = _case_job(golden, ci)
     full, early, direct = P.render(job)

@@ -137,6 +137,10 @@ CASES = [
     (22050, 0.12, 300, 17, [0.03, 0.03], (1.1, 5.5, 0.0), (5.0, 5.0, 3.0)),
     (44100, 0.08, 400, 19, [0.02], (1.4, 0.7, 0.4), (6.0, 4.0, 3.0)),
     (48000, 0.06, 512, 23, [0.04, 0.04], (1.2, 3.3, -0.2), (9.0, 8.0, 4.0)),
+    # sources a few cm from a mic: stage-1 taps before mid index 0 (head truncation)
+    (16000, 0.1, 64, 4, [0.04], (0.045, 0.0, 0.0), (4.0, 3.5, 2.8)),
+    (48000, 0.12, 128, 4, [0.1], (0.07, 0.0, 0.0), (4.0, 3.5, 2.8)),
+    (16000, 0.05, 0, 9, [0.04], (0.03, 0.0, 0.0), (4.0, 3.5, 2.8)),
 ]
 
 
