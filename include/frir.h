@@ -188,6 +188,9 @@ int32_t frir_launch_count(const frir_plan* plan, const frir_batch* batch, int32_
 
 const char* frir_last_error(void);
 int32_t frir_abi_version(void);
+/* Debug builds (-DFRIR_DEBUG): source line of the first failed in-kernel
+   bounds check since load, 0 if none (always 0 in release builds). */
+int32_t frir_debug_status(void);
 /* sizeof of frir_job (0), frir_batch (1), frir_plan_desc (2): lets bindings
    verify their struct mirrors. */
 int64_t frir_struct_size(int32_t which);

@@ -88,6 +88,7 @@ SIGNATURES = [
     ("frir_last_error", ctypes.c_char_p, []),
     ("frir_abi_version", c_int32, []),
     ("frir_struct_size", c_int64, [c_int32]),
+    ("frir_debug_status", c_int32, []),
 ]
 
 _lib = None

@@ -39,21 +39,27 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile libfrir.so if any source is newer than it."""
-    if not force and not _stale():
+DEBUG_OUT = PKG / "lib" / "libfrir_debug.so"
+
+
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> Path:
+    """Compile libfrir.so (or, with debug=True, libfrir_debug.so whose kernels
+    trap on out-of-range indices; load it with FRIR_LIB=...) if stale."""
+    out = DEBUG_OUT if debug else OUT
+    if not force and not debug and not _stale():
         return OUT
-    OUT.parent.mkdir(parents=True, exist_ok=True)
-    tmp = OUT.with_suffix(".so.tmp")
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", str(tmp), *[str(CSRC / s) for s in SOURCES]]
+    out.parent.mkdir(parents=True, exist_ok=True)
+    tmp = out.with_suffix(".so.tmp")
+    flags = NVCC_FLAGS + (["-DFRIR_DEBUG"] if debug else [])
+    cmd = [_nvcc(), *flags, "-o", str(tmp), *[str(CSRC / s) for s in SOURCES]]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed:\n{res.stdout}\n{res.stderr}")
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, debug="--debug" in sys.argv))

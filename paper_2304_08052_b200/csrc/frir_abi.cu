@@ -68,6 +68,8 @@ extern "C" {
 const char* frir_last_error(void) { return g_err.c_str(); }
 int32_t frir_abi_version(void) { return FRIR_ABI_VERSION; }
 
+int32_t frir_debug_status(void) { return check_line(); }
+
 int64_t frir_struct_size(int32_t which) {
   switch (which) {
     case 0: return (int64_t)sizeof(frir_job);

@@ -59,4 +59,5 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* ws, size_t
                     int stages);
 size_t workspace_bytes(const frir_batch* b);
 int launches(const frir_batch* b, int early);
+int check_line();
 }  // namespace frir

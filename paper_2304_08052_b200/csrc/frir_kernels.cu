@@ -17,6 +17,20 @@
 #include "frir_internal.h"
 #include "frir_philox.cuh"
 
+// Debug builds (-DFRIR_DEBUG, build.py --debug) trap on any out-of-range
+// table/item/output index; compute-sanitizer is not available on the pool.
+__device__ int g_frir_check_line = 0;  // first failed FRIR_CHECK (debug builds)
+#ifdef FRIR_DEBUG
+#define FRIR_CHECK(cond)                                 \
+  do {                                                   \
+    if (!(cond)) g_frir_check_line = __LINE__;           \
+  } while (0)
+#else
+#define FRIR_CHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 namespace frir {
 namespace {
 
@@ -188,6 +202,7 @@ __global__ void __launch_bounds__(128) geom_kernel(GeomArgs A) {
       if (k < nk) {
         double D;
         int q = delay_of(px[k], py[k], pz[k], mics + 3 * m, J.c0, A.rate, rate_c0, J.L, &D);
+        FRIR_CHECK(q >= 0 && q < J.L && r0 + k < rows);
         out[k] = make_item(q, lg[k] / (float)D, A.r_h, A.t0, A.rh_magic);
       }
     }
@@ -273,6 +288,7 @@ __global__ void __launch_bounds__(kSortThreads) sort_kernel(SortArgs A) {
     const int rank = __popc(peers & ((1u << lane) - 1u));
     unsigned short* slot = s_cnt + (ok ? b * kSortWarps + warp : 0);
     const int pos = ok ? *slot + rank : 0;
+    FRIR_CHECK(!ok || (pos >= 0 && pos < rows && b < nbk));
     __syncwarp();
     if (ok) {
       items[pos] = v;
@@ -539,6 +555,7 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A)
         if ((valid & 1) && khi < n1 && !head_item) {
           const int rho = e - down * khi;
           const int mm = n1 - 1 - khi;
+          FRIR_CHECK(mm >= 0 && (mm >> 7) < nphi && rho >= 0 && rho < down);
           const double2 lo = s_plo[mm & 127], hi = s_phi[mm >> 7], zr = s_zph[rho];
           const Cplx pm = cmul({hi.x, hi.y}, {lo.x, lo.y});
           const Cplx t = cmul(pm, {zr.x, zr.y});
@@ -566,6 +583,8 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A)
           for (int k = klo + lane; k < kend; k += 32) {
             const int mm = n1 - 1 - k;
             if (mm >= d.horizon) continue;
+            FRIR_CHECK(down * k + half1 - up * qs >= 0 && down * k + half1 - up * qs < d.len1);
+            FRIR_CHECK((mm >> 7) < nphi);
             const double cc = (double)as * A.plan.h1up[down * k + half1 - up * qs];
             const double2 lo = s_plo[mm & 127], hi = s_phi[mm >> 7];
             const Cplx pm = cmul({hi.x, hi.y}, {lo.x, lo.y});
@@ -619,6 +638,7 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A)
       const int e = d.r_l * n + d.half2 - n1;
       const bool act = n < n2 && e >= 0 && e < d.half2;
       if (act) {
+        FRIR_CHECK(e >= 0 && e < d.half2);
         corrF = A.plan.kappa[2 * e] * sF0 + A.plan.kappa[2 * e + 1] * sF1;
         if (EARLY) corrE = A.plan.kappa[2 * e] * sE0 + A.plan.kappa[2 * e + 1] * sE1;
       }
@@ -719,6 +739,7 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A)
       nxt = pn < rows ? items[pn] : make_int2(0xFFFFF, 0);  // prefetch the next batch
       const int bk = (mine.x & 0xFFFFF) >> 5;
       const unsigned dec = (((unsigned)mine.x >> 20) & 0x3FFu) * (512u * NBK) + 8u * (32u - (mine.x & 31));
+      FRIR_CHECK(p + lane >= rows || (((unsigned)mine.x >> 20) & 0x3FFu) < (unsigned)r_h);
       __syncwarp();
       s_it[lane] = make_int2((int)dec, mine.y);
       __syncwarp();
@@ -745,6 +766,7 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A)
               const int n = np - kExt;
               double cd = 0.0, cw = 0.0;
               for (int k = klo; k < 0; ++k) {
+                FRIR_CHECK(down * k + half1 - up * qs >= 0 && down * k + half1 - up * qs < d.len1);
                 const double cc = as * A.plan.h1up[down * k + half1 - up * qs];
                 const int idx = d.r_l * n + d.half2 - k;
                 if (idx >= 0 && idx < d.len2) cd += cc * A.plan.h2[idx];
@@ -790,6 +812,12 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A)
 }  // namespace
 
 // ---------------------------------------------------------------- host launcher
+int check_line() {
+  int v = 0;
+  cudaMemcpyFromSymbol(&v, g_frir_check_line, sizeof(int));
+  return v;
+}
+
 size_t workspace_bytes(const frir_batch* b) {
   return align_up((size_t)b->total_items * 8) + align_up((size_t)b->total_channels * 4) + 256;
 }
