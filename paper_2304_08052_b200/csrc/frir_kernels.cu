@@ -310,7 +310,7 @@ struct RenderArgs {
   float* out_early;
 };
 
-constexpr int kRenderThreads = 256;
+constexpr int kRenderThreads = 384;  // 12 warps: the shared tables amortise over more warps
 constexpr int kWarps = kRenderThreads / 32;
 __device__ __forceinline__ int ceil_div_i(int a, int b) {  // b > 0, any sign of a
   return a >= 0 ? (a + b - 1) / b : -((-a) / b);
@@ -463,7 +463,7 @@ struct Channel {
 };
 
 template <bool EARLY, int NBK>
-__global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A) {
+__global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(RenderArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const frir_plan_desc& d = A.plan.d;
   constexpr int kRow = 64 * NBK;  // doubled rows (see Channel::add)
@@ -474,7 +474,9 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A)
   double* s_corr_all = s_scan + kScanSmem;                                 // [warp][V][32]
   float* s_tile = reinterpret_cast<float*>(s_corr_all + kWarps * V * 32);  // [warp][V][D, W][kTile]
   int2* s_items = reinterpret_cast<int2*>(s_tile + (size_t)kWarps * V * 2 * kTile);
-  float* s_head = reinterpret_cast<float*>(s_items + 32 * kWarps);        // [warp][V][D, W][64]
+  double4* s_zeta = reinterpret_cast<double4*>(s_items + 32 * kWarps);   // [warp][32]
+  double* s_xt = reinterpret_cast<double*>(s_zeta + 32 * kWarps);         // [warp][F, E][64]
+  float* s_head = reinterpret_cast<float*>(s_xt + 128 * kWarps);          // [warp][V][D, W][64]
   double2* s_plo = reinterpret_cast<double2*>(s_head + kWarps * V * 2 * 64);  // p^i, i < 128
   double2* s_zph = s_plo + 128;                                         // Z[rho], rho < down
   double2* s_phi = s_zph + d.down;                                      // p^(128 j)
@@ -497,6 +499,8 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A)
   double* corrE_s = corrF_s + 32;
   int2* s_it = s_items + 32 * warp;
   float* head_s = s_head + warp * V * 2 * 64;
+  double4* zeta_s = s_zeta + 32 * warp;
+  double* xt_s = s_xt + 128 * warp;
   const double c1 = A.plan.lp[0], c2 = A.plan.lp[1];
   const Cplx v0a = {A.plan.lp[2], A.plan.lp[3]}, v0b = {A.plan.lp[4], A.plan.lp[5]};
   const int sup = d.sup, r_h = d.r_h, up = d.up, down = d.down, half1 = d.half1;
@@ -520,140 +524,13 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A)
     float* outF = A.out_full + J.out_off + (size_t)m * J.out_stride;
     float* outE = EARLY ? A.out_early + J.out_off + (size_t)m * J.out_stride : nullptr;
 
-    // ---- tail: HP state at n1 (modal sum) + taps past n1 (resample.py:107-113 truncation)
-    // Items are bucket-sorted, so the ones within the HP memory horizon of n1
-    // are a suffix of the list; each lane takes one item per step (32 at a time,
-    // next chunk prefetched), FP64 complex accumulation, fixed reduction order.
-    Cplx zF = {0.0, 0.0}, zE = {0.0, 0.0};
-    double xtF[2] = {0.0, 0.0}, xtE[2] = {0.0, 0.0};
-    {
-      const int kthr = n1 - d.horizon;  // need k_hi >= kthr
-      int base = rows;
-      int2 nx = base - 32 + lane >= 0 ? items[base - 32 + lane] : make_int2(0, 0);
-      for (; base > 0; base -= 32) {
-        const int r = base - 32 + lane;
-        const int2 it = nx;
-        nx = r - 32 >= 0 ? items[r - 32] : make_int2(0, 0);  // prefetch the previous chunk
-        int q = 0, valid = 0, khi = -1, e = 0;
-        bool early = false;
-        float a = 0.f;
-        if (r >= 0) {
-          const int spb = it.x & 0xFFFFF;
-          const int phi = ((unsigned)it.x >> 20) & 0x3FF;
-          const float ae = __int_as_float(it.y);
-          early = ae < 0.f;
-          a = fabsf(ae);
-          q = r_h * (spb - kSpBias - kExt) - d.t0 - phi;
-          e = up * q + half1;  // >= 0
-          khi = (int)__umulhi((unsigned)e, down_magic);
-          valid = khi >= kthr;
-          // every item of this bucket or below has q <= qmax: stop when past the horizon
-          const int qmax = r_h * ((spb | 31) - kSpBias - kExt) - d.t0;
-          if ((int)__umulhi((unsigned)(up * qmax + half1), down_magic) >= kthr) valid |= 2;
-        }
-        const bool head_item = (valid & 1) && e < 2 * half1;  // some stage-1 taps at k < 0
-        if ((valid & 1) && khi < n1 && !head_item) {
-          const int rho = e - down * khi;
-          const int mm = n1 - 1 - khi;
-          FRIR_CHECK(mm >= 0 && (mm >> 7) < nphi && rho >= 0 && rho < down);
-          const double2 lo = s_plo[mm & 127], hi = s_phi[mm >> 7], zr = s_zph[rho];
-          const Cplx pm = cmul({hi.x, hi.y}, {lo.x, lo.y});
-          const Cplx t = cmul(pm, {zr.x, zr.y});
-          zF.re = fma((double)a, t.re, zF.re);
-          zF.im = fma((double)a, t.im, zF.im);
-          if (EARLY && early) {
-            zE.re = fma((double)a, t.re, zE.re);
-            zE.im = fma((double)a, t.im, zE.im);
-          }
-        }
-        // straddlers (taps on both sides of n1) and head items (taps before 0):
-        // one at a time in lane order, explicit taps
-        unsigned strad = __ballot_sync(0xffffffffu, (valid & 1) && (khi >= n1 || head_item));
-        while (strad) {
-          const int src = __ffs(strad) - 1;
-          strad &= strad - 1;
-          const int qs = __shfl_sync(0xffffffffu, q, src);
-          const float as = __shfl_sync(0xffffffffu, a, src);
-          const bool es = __shfl_sync(0xffffffffu, (int)early, src) != 0;
-          const int khs = (int)__umulhi((unsigned)(up * qs + half1), down_magic);
-          const int xs = up * qs - half1 + 1024 * down;  // >= 0 (half1 = 10 r_h <= 1024 down)
-          const int klo = max(0, (int)__umulhi((unsigned)xs, down_magic) - 1024 + (xs % down != 0));
-          // taps 0 <= k <= min(k_hi, n1 - 1) feed the state (strided over lanes)
-          const int kend = min(khs + 1, n1);
-          for (int k = klo + lane; k < kend; k += 32) {
-            const int mm = n1 - 1 - k;
-            if (mm >= d.horizon) continue;
-            FRIR_CHECK(down * k + half1 - up * qs >= 0 && down * k + half1 - up * qs < d.len1);
-            FRIR_CHECK((mm >> 7) < nphi);
-            const double cc = (double)as * A.plan.h1up[down * k + half1 - up * qs];
-            const double2 lo = s_plo[mm & 127], hi = s_phi[mm >> 7];
-            const Cplx pm = cmul({hi.x, hi.y}, {lo.x, lo.y});
-            zF.re = fma(cc, pm.re, zF.re);
-            zF.im = fma(cc, pm.im, zF.im);
-            if (EARLY && es) {
-              zE.re = fma(cc, pm.re, zE.re);
-              zE.im = fma(cc, pm.im, zE.im);
-            }
-          }
-          // taps k >= n1: input past the truncation point
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int l = lane + 32 * h;
-            const int k = n1 + l;
-            if (l < d.lt_max && k <= khs) {
-              const int idx = down * k + half1 - up * qs;
-              if (idx >= 0 && idx < d.len1) {
-                const double cc = (double)as * A.plan.h1up[idx];
-                xtF[h] += cc;
-                if (EARLY && es) xtE[h] += cc;
-              }
-            }
-          }
-        }
-        if (!__any_sync(0xffffffffu, valid & 2)) break;
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      zF.re += __shfl_xor_sync(0xffffffffu, zF.re, o);
-      zF.im += __shfl_xor_sync(0xffffffffu, zF.im, o);
-      if (EARLY) {
-        zE.re += __shfl_xor_sync(0xffffffffu, zE.re, o);
-        zE.im += __shfl_xor_sync(0xffffffffu, zE.im, o);
-      }
-    }
-    // state s = 2 Re(v0 zeta); corrections for outputs n >= n_c (<= 10 of them)
+    // ---- tail state (truncation at n1, resample.py:107-113): per-lane partial
+    // modal sums and the taps past n1 accumulate in smem while the items are
+    // staged (the items within the HP horizon are a suffix of the sorted list)
     const int n_c = n1 - d.half2 > 0 ? (n1 - d.half2 + d.r_l - 1) / d.r_l : 0;
-    {
-      double corrF = 0.0, corrE = 0.0;
-      Cplx ta = cmul(v0a, zF), tb = cmul(v0b, zF);
-      double sF0 = 2.0 * ta.re, sF1 = 2.0 * tb.re;
-      double sE0 = 0.0, sE1 = 0.0;
-      if (EARLY) {
-        Cplx ea = cmul(v0a, zE), eb = cmul(v0b, zE);
-        sE0 = 2.0 * ea.re;
-        sE1 = 2.0 * eb.re;
-      }
-      const int n = n_c + lane;
-      const int e = d.r_l * n + d.half2 - n1;
-      const bool act = n < n2 && e >= 0 && e < d.half2;
-      if (act) {
-        FRIR_CHECK(e >= 0 && e < d.half2);
-        corrF = A.plan.kappa[2 * e] * sF0 + A.plan.kappa[2 * e + 1] * sF1;
-        if (EARLY) corrE = A.plan.kappa[2 * e] * sE0 + A.plan.kappa[2 * e + 1] * sE1;
-      }
-      for (int l = 0; l < d.lt_max; ++l) {
-        double xf = shfl_d(xtF[l >> 5], l & 31);
-        double xe = EARLY ? shfl_d(xtE[l >> 5], l & 31) : 0.0;
-        if (act && l <= e) {
-          double uu = A.plan.u[e - l];
-          corrF += xf * uu;
-          if (EARLY) corrE += xe * uu;
-        }
-      }
-      corrF_s[lane] = corrF;
-      if (EARLY) corrE_s[lane] = corrE;
-    }
+    const int kthr = n1 - d.horizon;  // items with k_hi >= kthr feed the state
+    zeta_s[lane] = make_double4(0.0, 0.0, 0.0, 0.0);
+    xt_s[lane] = 0.0; xt_s[32 + lane] = 0.0; xt_s[64 + lane] = 0.0; xt_s[96 + lane] = 0.0;
     // windows touched by early items (q in [q0 - lo, q0 + hi], core.py:257-264)
     int ew_lo = 0, ew_hi = -1;
     if (EARLY) {
@@ -744,6 +621,113 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(RenderArgs A)
       s_it[lane] = make_int2((int)dec, mine.y);
       __syncwarp();
       const int cnt = min(32, rows - p);
+      {  // tail: this batch's contribution to the HP state at n1
+        const int spb = mine.x & 0xFFFFF;
+        const int qm = r_h * (spb - kSpBias - kExt) - d.t0 - (((unsigned)mine.x >> 20) & 0x3FF);
+        const int e = up * qm + half1;  // >= 0
+        const int khi = (int)__umulhi((unsigned)e, down_magic);
+        const bool valid = lane < cnt && khi >= kthr;
+        if (__any_sync(0xffffffffu, valid)) {
+          const float ae = __int_as_float(mine.y);
+          const bool early = ae < 0.f;
+          const double a = fabs((double)ae);
+          const bool head_item = e < 2 * half1;  // some stage-1 taps at k < 0
+          double4 z = zeta_s[lane];
+          if (valid && khi < n1 && !head_item) {
+            const int rho = e - down * khi;
+            const int mm = n1 - 1 - khi;
+            FRIR_CHECK(mm >= 0 && (mm >> 7) < nphi && rho >= 0 && rho < down);
+            const double2 lo = s_plo[mm & 127], hi = s_phi[mm >> 7], zr = s_zph[rho];
+            const Cplx t = cmul(cmul({hi.x, hi.y}, {lo.x, lo.y}), {zr.x, zr.y});
+            z.x = fma(a, t.re, z.x);
+            z.y = fma(a, t.im, z.y);
+            if (EARLY && early) {
+              z.z = fma(a, t.re, z.z);
+              z.w = fma(a, t.im, z.w);
+            }
+          }
+          // straddlers (taps on both sides of n1) and head items: one at a time
+          unsigned strad = __ballot_sync(0xffffffffu, valid && (khi >= n1 || head_item));
+          while (strad) {
+            const int src = __ffs(strad) - 1;
+            strad &= strad - 1;
+            const int qs = __shfl_sync(0xffffffffu, qm, src);
+            const float aes = __int_as_float(__shfl_sync(0xffffffffu, mine.y, src));
+            const double as = fabs((double)aes);
+            const bool es = aes < 0.f;
+            const int khs = (int)__umulhi((unsigned)(up * qs + half1), down_magic);
+            const int xs = up * qs - half1 + 1024 * down;  // >= 0 (half1 = 10 r_h <= 1024 down)
+            const int klo = max(0, (int)__umulhi((unsigned)xs, down_magic) - 1024 + (xs % down != 0));
+            const int kend = min(khs + 1, n1);
+            for (int k = klo + lane; k < kend; k += 32) {  // taps 0 <= k < n1 feed the state
+              const int mm = n1 - 1 - k;
+              if (mm >= d.horizon) continue;
+              FRIR_CHECK(down * k + half1 - up * qs >= 0 && down * k + half1 - up * qs < d.len1);
+              const double cc = as * A.plan.h1up[down * k + half1 - up * qs];
+              const double2 lo = s_plo[mm & 127], hi = s_phi[mm >> 7];
+              const Cplx pm = cmul({hi.x, hi.y}, {lo.x, lo.y});
+              z.x = fma(cc, pm.re, z.x);
+              z.y = fma(cc, pm.im, z.y);
+              if (EARLY && es) {
+                z.z = fma(cc, pm.re, z.z);
+                z.w = fma(cc, pm.im, z.w);
+              }
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {  // taps k >= n1: input past the truncation point
+              const int l = lane + 32 * h;
+              const int k = n1 + l;
+              if (l < d.lt_max && k <= khs) {
+                const int idx = down * k + half1 - up * qs;
+                if (idx >= 0 && idx < d.len1) {
+                  const double cc = as * A.plan.h1up[idx];
+                  xt_s[l] += cc;
+                  if (EARLY && es) xt_s[64 + l] += cc;
+                }
+              }
+            }
+          }
+          zeta_s[lane] = z;
+        }
+        if (p + 32 >= rows) {  // every item staged: finish the state and the corrections
+          double4 z = zeta_s[lane];
+          Cplx zF = {z.x, z.y}, zE = {z.z, z.w};
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            zF.re += __shfl_xor_sync(0xffffffffu, zF.re, o);
+            zF.im += __shfl_xor_sync(0xffffffffu, zF.im, o);
+            if (EARLY) {
+              zE.re += __shfl_xor_sync(0xffffffffu, zE.re, o);
+              zE.im += __shfl_xor_sync(0xffffffffu, zE.im, o);
+            }
+          }
+          __syncwarp();
+          double corrF = 0.0, corrE = 0.0;
+          const Cplx ta = cmul(v0a, zF), tb = cmul(v0b, zF);  // s = 2 Re(v0 zeta)
+          const double s0 = 2.0 * ta.re, s1 = 2.0 * tb.re;
+          double se0 = 0.0, se1 = 0.0;
+          if (EARLY) {
+            const Cplx ea = cmul(v0a, zE), eb = cmul(v0b, zE);
+            se0 = 2.0 * ea.re;
+            se1 = 2.0 * eb.re;
+          }
+          const int n = n_c + lane;
+          const int ee = d.r_l * n + d.half2 - n1;
+          const bool act = n < n2 && ee >= 0 && ee < d.half2;
+          if (act) {
+            corrF = A.plan.kappa[2 * ee] * s0 + A.plan.kappa[2 * ee + 1] * s1;
+            if (EARLY) corrE = A.plan.kappa[2 * ee] * se0 + A.plan.kappa[2 * ee + 1] * se1;
+            for (int l = 0; l < d.lt_max && l <= ee; ++l) {
+              const double uu = A.plan.u[ee - l];
+              corrF += xt_s[l] * uu;
+              if (EARLY) corrE += xt_s[64 + l] * uu;
+            }
+          }
+          corrF_s[lane] = corrF;
+          if (EARLY) corrE_s[lane] = corrE;
+          __syncwarp();
+        }
+      }
       {  // head: stage-1 taps at mid index < 0 do not exist in the reference (resample.py:107)
         const int qm = r_h * ((mine.x & 0xFFFFF) - kSpBias - kExt) - d.t0 - (((unsigned)mine.x >> 20) & 0x3FF);
         unsigned hm = __ballot_sync(0xffffffffu, lane < cnt && up * qm < half1);
@@ -828,7 +812,8 @@ static size_t render_smem(const frir_plan_desc& d, bool early) {
   const int v = early ? 2 : 1;
   return (size_t)d.r_h * 64 * table_blocks(d) * 8 + kScanSmem * 8 + (size_t)kWarps * v * 32 * 8 +
          (size_t)kWarps * v * 2 * kTile * 4 + (size_t)kWarps * 32 * 8 +
-         (size_t)kWarps * v * 2 * 64 * 4 + (size_t)(128 + d.down + d.horizon / 128 + 1) * 16;
+         (size_t)kWarps * v * 2 * 64 * 4 + (size_t)(128 + d.down + d.horizon / 128 + 1) * 16 +
+         (size_t)kWarps * (32 * 32 + 128 * 8);
 }
 
 template <bool EARLY, int NBK>
