@@ -297,7 +297,7 @@ def run_ours(args):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cores = len(os.sched_getaffinity(0))
-        n_cpu = args.cpu_jobs or {1: 1, 2: 64, 3: 48, 4: 4, 5: 32}[cfg]
+        n_cpu = args.cpu_jobs or {1: 1, 2: 192, 3: 96, 4: 16, 5: 128}[cfg]
         rate, nj, walls = cpu_oracle_rate(cfg, n_cpu, cores)
         cpu = {"value": rate, "unit": "RIR/s", "cores": cores, "kind": "port",
                "sample": f"first {nj} jobs of config {cfg}, oracle/framrir_port.py (numpy+scipy, the reference's "
