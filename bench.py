@@ -324,7 +324,8 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "RIR/s", "h2d_bytes_per_step": e2e["h2d"],
                 "d2h_bytes_per_step": e2e["d2h"], "ms_per_step": e2e_ms,
-                "path": "frir_jobs_prepare + H2D(job table) + frir_simulate + D2H(all RIRs), pinned host"},
+                "path": "engine.HostPipeline: frir_jobs_prepare + H2D(job tables) + frir_simulate + "
+                        "D2H(all RIRs) to pinned host, 4 chunks, copy overlapped with render"},
         "gpu_launches": launches_per_step * K,
         "clocks": sampler.summary(),
     }
@@ -332,43 +333,28 @@ def run_ours(args):
 
 
 def run_e2e(args, batch, early, dev, stream):
-    """Same metric through the C-ABI with host buffers: host validation/layout,
-    H2D of the job tables, render, D2H of every RIR into pinned memory."""
-    import torch
-
+    """Same metric through the public host-output API (engine.HostPipeline):
+    host validation/layout of the job tables, H2D, render, D2H of every RIR
+    into pinned memory, with the copy of chunk k overlapping the render of
+    chunk k + 1."""
     from paper_2304_08052_b200 import engine
 
-    w, pb0, _ = batch
+    w = batch[0]
     steps = max(2, min(args.steps, 10))
-    pinned_jobs = torch.empty(pb0.jobs.nbytes, dtype=torch.uint8).pin_memory()
-    pinned_full = torch.empty(int(pb0.batch.total_out), dtype=torch.float32).pin_memory()
-    pinned_early = torch.empty(int(pb0.batch.total_out), dtype=torch.float32).pin_memory() if early else None
-    pinned_direct = torch.empty(int(pb0.batch.total_channels), dtype=torch.int32).pin_memory()
-    db = engine.DeviceBatch(pb0, device=dev)
-    full, earlyb, direct = db.alloc_outputs(early)
-    h2d = pb0.jobs.nbytes + pb0.chan_job.nbytes + pb0.chan_order.nbytes + pb0.mics.nbytes
-    d2h = pinned_full.numel() * 4 * (2 if early else 1) + pinned_direct.numel() * 4
-
-    def one():
-        pb = engine.prepare(w.sample_rate, w.jobs, w.mics)  # host validation + layout (C)
-        pinned_jobs.numpy()[:] = pb.jobs.view(np.uint8).reshape(-1)
-        db.jobs.copy_(pinned_jobs, non_blocking=True)
-        db.chan_job.copy_(torch.from_numpy(pb.chan_job), non_blocking=True)
-        db.chan_order.copy_(torch.from_numpy(pb.chan_order), non_blocking=True)
-        db.mics.copy_(torch.from_numpy(pb.mics.reshape(-1)), non_blocking=True)
-        db.launch(full, earlyb, direct, stream)
-        pinned_full.copy_(full, non_blocking=True)
-        if early:
-            pinned_early.copy_(earlyb, non_blocking=True)
-        pinned_direct.copy_(direct, non_blocking=True)
-        torch.cuda.synchronize(dev)
-
-    one()
+    pipe = engine.HostPipeline(w.sample_rate, w.jobs, w.mics, include_early=early, chunks=4, device=dev)
+    pipe.run()
+    torch_sync(dev)
     t0 = time.perf_counter()
     for _ in range(steps):
-        one()
+        pipe.run()
     ms = (time.perf_counter() - t0) * 1e3 / steps
-    return {"ms_per_step": ms, "h2d": int(h2d), "d2h": int(d2h)}
+    return {"ms_per_step": ms, "h2d": int(pipe.h2d_bytes), "d2h": int(pipe.d2h_bytes)}
+
+
+def torch_sync(dev):
+    import torch
+
+    torch.cuda.synchronize(dev)
 
 
 # ---------------------------------------------------------------- reference arm

@@ -200,3 +200,87 @@ def simulate_jobs(sample_rate: int, jobs: np.ndarray, mics: np.ndarray, include_
     """Validate, upload and render a job table; returns device tensors."""
     pb = prepare(sample_rate, jobs, mics, padded=padded, draws=draws)
     return DeviceBatch(pb, device=device).run(include_early)
+
+
+class HostPipeline:
+    """Batched generation straight into pinned host memory (the e2e path).
+
+    The job table is split into ``chunks`` sub-batches that are validated and
+    laid out once; every ``run()`` copies the job tables host->device, renders
+    chunk k on a compute stream while chunk k-1's RIRs stream device->host on a
+    copy stream, and returns flat float32 host arrays (full, early) plus the
+    per-channel direct indices, laid out as ``self.layout`` describes.
+    """
+
+    def __init__(self, sample_rate: int, jobs: np.ndarray, mics: np.ndarray,
+                 include_early: bool = True, chunks: int = 4, device=None):
+        require_cuda()
+        n = len(jobs)
+        chunks = max(1, min(chunks, n))
+        bounds = [n * i // chunks for i in range(chunks + 1)]
+        self.sample_rate = sample_rate
+        self.include_early = include_early
+        self.dev = torch.device("cuda", torch.cuda.current_device() if device is None
+                                else torch.device(device).index)
+        self.parts = []
+        for lo, hi in zip(bounds[:-1], bounds[1:]):
+            pb = prepare(sample_rate, jobs[lo:hi], mics)
+            db = DeviceBatch(pb, device=self.dev)
+            full, early, direct = db.alloc_outputs(include_early)
+            nfl = int(pb.batch.total_out)
+            host = {
+                "jobs": torch.empty(pb.jobs.nbytes, dtype=torch.uint8).pin_memory(),
+                "full": torch.empty(nfl, dtype=torch.float32).pin_memory(),
+                "early": torch.empty(nfl, dtype=torch.float32).pin_memory() if include_early else None,
+                "direct": torch.empty(int(pb.batch.total_channels), dtype=torch.int32).pin_memory(),
+            }
+            self.parts.append((lo, hi, pb, db, (full, early, direct), host))
+        self.compute = torch.cuda.Stream(self.dev)
+        self.copy = torch.cuda.Stream(self.dev)
+        self.jobs_src = jobs
+        self.mics_src = mics
+
+    @property
+    def h2d_bytes(self) -> int:
+        return sum(p[2].jobs.nbytes + p[2].chan_job.nbytes + p[2].chan_order.nbytes + p[2].mics.nbytes
+                   for p in self.parts)
+
+    @property
+    def d2h_bytes(self) -> int:
+        v = 2 if self.include_early else 1
+        return sum(p[5]["full"].numel() * 4 * v + p[5]["direct"].numel() * 4 for p in self.parts)
+
+    def job_view(self, j: int, kind: str = "full") -> np.ndarray:
+        """(M, n2) host view of job j after run()."""
+        for lo, hi, pb, _, _, host in self.parts:
+            if lo <= j < hi:
+                J = pb.jobs[j - lo]
+                m, stride, n2, off = int(J["n_mics"]), int(J["out_stride"]), int(J["n2"]), int(J["out_off"])
+                return host[kind].numpy()[off: off + m * stride].reshape(m, stride)[:, :n2]
+        raise IndexError(j)
+
+    def run(self, revalidate: bool = True):
+        """One end-to-end pass; returns the list of per-chunk host buffers."""
+        done = []
+        for lo, hi, pb, db, (full, early, direct), host in self.parts:
+            if revalidate:  # host validation + layout, as a caller with fresh rooms would do
+                pb = prepare(self.sample_rate, self.jobs_src[lo:hi], self.mics_src)
+            host["jobs"].numpy()[:] = pb.jobs.view(np.uint8).reshape(-1)
+            with torch.cuda.stream(self.compute):
+                db.jobs.copy_(host["jobs"], non_blocking=True)
+                db.chan_job.copy_(torch.from_numpy(pb.chan_job), non_blocking=True)
+                db.chan_order.copy_(torch.from_numpy(pb.chan_order), non_blocking=True)
+                db.mics.copy_(torch.from_numpy(pb.mics.reshape(-1)), non_blocking=True)
+                db.launch(full, early, direct, self.compute)
+                ev = torch.cuda.Event()
+                ev.record(self.compute)
+            with torch.cuda.stream(self.copy):
+                self.copy.wait_event(ev)
+                host["full"].copy_(full, non_blocking=True)
+                if early is not None:
+                    host["early"].copy_(early, non_blocking=True)
+                host["direct"].copy_(direct, non_blocking=True)
+            done.append(host)
+        self.copy.synchronize()
+        self.compute.synchronize()
+        return done

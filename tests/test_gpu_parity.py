@@ -170,6 +170,18 @@ def test_bit_reproducible_and_layout_invariant():
             assert torch.equal(a.job_view(j, "early"), half.job_view(j - 12, "early"))
 
 
+def test_host_pipeline_equals_device_batch():
+    w = workloads.config2(10)
+    ref = engine.simulate_jobs(16000, w.jobs, w.mics, include_early=True)
+    pipe = engine.HostPipeline(16000, w.jobs, w.mics, include_early=True, chunks=3)
+    for _ in range(2):  # repeated runs reuse the buffers
+        pipe.run()
+        for j in range(10):
+            assert np.array_equal(pipe.job_view(j), ref.job_view(j).cpu().numpy())
+            assert np.array_equal(pipe.job_view(j, "early"), ref.job_view(j, "early").cpu().numpy())
+    assert pipe.d2h_bytes > 0 and pipe.h2d_bytes > 0
+
+
 def test_full_only_equals_full_of_both():
     w = workloads.config2(8)
     both = engine.simulate_jobs(16000, w.jobs, w.mics, include_early=True)
