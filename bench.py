@@ -195,10 +195,14 @@ def run_ours(args):
     from paper_2304_08052_b200 import _abi, engine, workloads
 
     rank, world, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())  # --dist-backend gloo may share one GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:  # CPU collectives: lets N ranks share a GPU for testing the multi-rank path
+            dist.init_process_group("gloo")
     cfg = args.config
     early = not args.no_early
     variants = 2 if early else 1
@@ -259,8 +263,9 @@ def run_ours(args):
     render_ms = [sum(e[1].elapsed_time(e[2]) for e in ev[k]) for k in range(K)]
     tot_ms = float(sum(step_ms))
     tot_render = float(sum(render_ms))
-    t = torch.tensor([tot_ms, tot_render], dtype=torch.float64, device=dev)
-    n = torch.tensor([float(n_rirs_rank)], dtype=torch.float64, device=dev)
+    cdev = dev if args.dist_backend == "nccl" else torch.device("cpu")
+    t = torch.tensor([tot_ms, tot_render], dtype=torch.float64, device=cdev)
+    n = torch.tensor([float(n_rirs_rank)], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(n, op=dist.ReduceOp.SUM)
@@ -271,7 +276,7 @@ def run_ours(args):
     # ---- end to end through the C-ABI with host buffers (rank-local, first shard)
     e2e = run_e2e(args, batches[0], early, dev, stream)
     if world > 1:
-        te = torch.tensor([e2e["ms_per_step"]], dtype=torch.float64, device=dev)
+        te = torch.tensor([e2e["ms_per_step"]], dtype=torch.float64, device=cdev)
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_ms = float(te[0])
     else:
@@ -394,6 +399,8 @@ def main():
     ap.add_argument("--no-early", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-jobs", type=int, default=None)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo lets several ranks share one GPU (testing the multi-rank path)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     line = run_reference(args) if args.impl == "reference" else run_ours(args)
