@@ -93,6 +93,11 @@ typedef struct {
   int32_t n_images;          /* I (SimParams.num_images), per job */
   int32_t mic_off;           /* first mic row in frir_batch.mics */
   int32_t n_mics;            /* M */
+  /* ---- extensions (defaults reproduce the reference) ---- */
+  int32_t n_images_hi;       /* > n_images: I ~ U{n_images..n_images_hi} from stream (seed, k, 2) */
+  int32_t normalize;         /* 0: reference scaling; 1: direct path of every channel = 1/1 m (x D_0m) */
+  double early_lo_ms;        /* early window [-lo, +hi] ms around the direct path; 0/0 means 6/50 */
+  double early_hi_ms;
   /* ---- layout (frir_jobs_prepare) ---- */
   int64_t img_off;           /* first image row (row 0 = direct path) */
   int64_t item_off;          /* first (image, mic) item */
@@ -107,6 +112,7 @@ typedef struct {
   double rr_max;             /* max_reflections, core.py:186-192 (0 when I == 0) */
   double alpha3, b3a3;       /* alpha**3 and beta**3 - alpha**3 (core.py:100) */
   double log2r;              /* log2(r): gains r**g are evaluated as exp2(g log2 r) in FP32 */
+  int32_t e_lo, e_hi;        /* early window in high-rate samples (core.py:257-258) */
   uint64_t key[4];          /* Philox keys of streams (seed, k, 0) and (seed, k, 1) */
 } frir_job;
 

@@ -146,9 +146,13 @@ def dense_train(q, amp, L):
     return x
 
 
-def early_only(x, q0, rate):
-    """[-6, +50] ms window around each channel's direct arrival, core.py:254-265."""
-    lo, hi = -(-6 * rate // 1000), -(-50 * rate // 1000)
+def early_only(x, q0, rate, window_ms=None):
+    """[-6, +50] ms window around each channel's direct arrival, core.py:254-265
+    (``window_ms`` restates the product's early-window extension for tests)."""
+    if window_ms is None:
+        lo, hi = -(-6 * rate // 1000), -(-50 * rate // 1000)
+    else:
+        lo, hi = math.ceil(window_ms[0] * rate / 1000.0), math.ceil(window_ms[1] * rate / 1000.0)
     idx = np.arange(x.shape[1])
     keep = (idx[None, :] >= (q0[:, None] - lo)) & (idx[None, :] <= (q0[:, None] + hi))
     return np.where(keep, x, 0.0)
@@ -165,7 +169,7 @@ def chain(x, fs):
     return signal.resample_poly(y, 1, r_l, axis=1, window=k2)
 
 
-def render(job: Job, draws: Draws | None = None, include_early: bool = True):
+def render(job: Job, draws: Draws | None = None, include_early: bool = True, early_window_ms=None):
     """Full (and early) RIR of one job: ``(full (M, n2), early or None, direct (M,))``."""
     if job.alpha == 0.0:
         raise ValueError("alpha must be > 0 to sample image distances")
@@ -177,7 +181,7 @@ def render(job: Job, draws: Draws | None = None, include_early: bool = True):
     full = chain(x, job.sample_rate)
     r_h, _ = factors(job.sample_rate)
     direct = np.clip(np.round(q[0] / r_h).astype(np.int64), 0, full.shape[1] - 1)
-    early = chain(early_only(x, q[0], rate), job.sample_rate) if include_early else None
+    early = chain(early_only(x, q[0], rate, early_window_ms), job.sample_rate) if include_early else None
     return full, early, direct
 
 

@@ -45,11 +45,13 @@ class FrirJob(ctypes.Structure):
         ("beta", c_double), ("perturb_lo", c_double), ("perturb_hi", c_double), ("tau", c_double),
         ("seed", c_uint64), ("source_index", c_int32), ("n_images", c_int32),
         ("mic_off", c_int32), ("n_mics", c_int32),
+        ("n_images_hi", c_int32), ("normalize", c_int32),
+        ("early_lo_ms", c_double), ("early_hi_ms", c_double),
         ("img_off", c_int64), ("item_off", c_int64), ("out_off", c_int64),
         ("chan_off", c_int32), ("out_stride", c_int32), ("L", c_int32), ("n1", c_int32),
         ("n2", c_int32), ("pad_", c_int32),
         ("r", c_double), ("rr_max", c_double), ("alpha3", c_double), ("b3a3", c_double),
-        ("log2r", c_double),
+        ("log2r", c_double), ("e_lo", c_int32), ("e_hi", c_int32),
         ("key", c_uint64 * 4),
     ]
 

@@ -53,6 +53,15 @@ def scene_fingerprint(scene: Scene) -> str:
     return hashlib.sha256(b"".join(p.tobytes() for p in parts)).hexdigest()[:16]
 
 
+def _extensions(params):
+    """(image range, early window or None, normalize) of a SimParams; works for
+    the reference's own SimParams too (no extension fields -> reference behaviour)."""
+    n = params.num_images
+    rng = (int(n[0]), int(n[1])) if isinstance(n, (tuple, list)) else (int(n), int(n))
+    window = tuple(getattr(params, "early_window_ms", (6.0, 50.0)))
+    return rng, (None if window == (6.0, 50.0) else window), getattr(params, "normalize", None)
+
+
 def _validate_sources(params: SimParams, scene: Scene, r: float) -> None:
     """Per-source checks in simulate_rir's order (core.py:140-148, 186-192, 209-210)."""
     srcs = np.atleast_2d(np.asarray(scene.sources, dtype=float))
@@ -62,7 +71,7 @@ def _validate_sources(params: SimParams, scene: Scene, r: float) -> None:
             raise ValueError("alpha must be > 0 to sample image distances")
         if c_max <= d0:
             raise ValueError(f"c0*t60 = {c_max:.3f} m must exceed the direct distance {d0:.3f} m")
-        if params.num_images > 0:
+        if _extensions(params)[0][1] > 0:
             rr = max_reflections(params.t60, float(d0), r, params.sound_speed)
             if rr < 1.0:
                 raise ValueError(f"rr_max must be >= 1, got {rr}")
@@ -84,7 +93,12 @@ def scene_jobs(params: SimParams, scene: Scene, seed=None):
     jobs["tau"] = params.tau
     jobs["seed"] = int(params.seed if seed is None else seed)
     jobs["source_index"] = np.arange(len(srcs))
-    jobs["n_images"] = int(params.num_images)
+    (lo, hi), window, normalize = _extensions(params)
+    jobs["n_images"] = lo
+    jobs["n_images_hi"] = hi if hi > lo else 0
+    if window is not None:
+        jobs["early_lo_ms"], jobs["early_hi_ms"] = window
+    jobs["normalize"] = 1 if normalize == "direct" else 0
     jobs["mic_off"] = 0
     jobs["n_mics"] = len(mics)
     return jobs, mics
@@ -123,6 +137,13 @@ def simulate_rir(params: SimParams, scene: Scene, include_early: bool = True, *,
     for k in range(len(srcs)):
         meta = dict(meta_base, source_index=k, distance=float(srcs[k, 0]),
                     azimuth=float(srcs[k, 1]), elevation=float(srcs[k, 2]))
+        (lo, hi), window, normalize = _extensions(params)
+        if hi > lo:
+            meta["num_images_drawn"] = int(pj[k]["n_images"])
+        if window is not None:
+            meta["early_window_ms"] = window
+        if normalize is not None:
+            meta["normalize"] = normalize
         meta.update(chain_meta)
         m, stride, n2, off = (int(pj[k][f]) for f in ("n_mics", "out_stride", "n2", "out_off"))
         ch = int(pj[k]["chan_off"])

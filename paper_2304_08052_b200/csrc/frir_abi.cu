@@ -211,6 +211,14 @@ int frir_jobs_prepare(int32_t sample_rate, frir_job* jobs, int32_t n_jobs, int32
   for (int32_t j = 0; j < n_jobs; ++j) {
     frir_job& J = jobs[j];
     std::string pre = "job " + std::to_string(j) + ": ";
+    // extension: I ~ U{n_images .. n_images_hi} from the job's own stream (seed, k, 2)
+    if (J.n_images_hi > J.n_images && J.n_images >= 0) {
+      uint64_t k2[2];
+      seed_keys(J.seed, (uint64_t)J.source_index, 2, k2);
+      const double u = u64_to_unit(stream_word(k2, 0));
+      J.n_images += (int32_t)(u * (double)(J.n_images_hi - J.n_images + 1));
+      J.n_images_hi = J.n_images;  // idempotent: a prepared table keeps its draw
+    }
     // SimParams.__post_init__ (params.py:49-65)
     if (!(J.t60 > 0)) { set_error(pre + "t60 must be > 0, got " + fmt("%g", J.t60)); return FRIR_EINVAL; }
     if (J.n_images < 0) { set_error(pre + "num_images must be >= 0"); return FRIR_EINVAL; }
@@ -253,6 +261,19 @@ int frir_jobs_prepare(int32_t sample_rate, frir_job* jobs, int32_t n_jobs, int32
       }
     }
     J.log2r = std::log2(J.r);
+    // early window (core.py:257-258: -ceil(6 rate / 1000) .. +ceil(50 rate / 1000))
+    if (J.early_lo_ms == 0.0 && J.early_hi_ms == 0.0) {
+      J.e_lo = (int32_t)((6 * rate + 999) / 1000);
+      J.e_hi = (int32_t)((50 * rate + 999) / 1000);
+    } else {
+      if (!(J.early_lo_ms >= 0.0 && J.early_hi_ms >= 0.0 && J.early_lo_ms < 1e6 && J.early_hi_ms < 1e6)) {
+        set_error(pre + "early window must be non-negative milliseconds");
+        return FRIR_EINVAL;
+      }
+      J.e_lo = (int32_t)std::ceil(J.early_lo_ms * (double)rate / 1000.0);
+      J.e_hi = (int32_t)std::ceil(J.early_hi_ms * (double)rate / 1000.0);
+    }
+    if (J.normalize < 0 || J.normalize > 1) { set_error(pre + "normalize must be 0 or 1"); return FRIR_EINVAL; }
     J.alpha3 = std::pow(J.alpha, 3.0);
     J.b3a3 = std::pow(J.beta, 3.0) - J.alpha3;
     uint64_t key[2];

@@ -41,6 +41,7 @@ constexpr double kPi = 3.141592653589793;          // np.pi/2 - (-np.pi/2)
 struct Workspace {
   int2* items;
   int* chan_q0;
+  float* chan_scale;
   int* counter;
 };
 
@@ -51,6 +52,7 @@ Workspace carve(void* base, const frir_batch* b) {
   Workspace w;
   w.items = (int2*)p; p += align_up((size_t)b->total_items * 8);
   w.chan_q0 = (int*)p; p += align_up((size_t)b->total_channels * 4);
+  w.chan_scale = (float*)p; p += align_up((size_t)b->total_channels * 4);
   w.counter = (int*)p;
   return w;
 }
@@ -127,6 +129,7 @@ __global__ void __launch_bounds__(128) geom_kernel(GeomArgs A) {
       int q = delay_of(x, y, z, mics + 3 * m, J.c0, A.rate, rate_c0, J.L, &D);
       items[(size_t)m * rows] = make_item(q, (float)__drcp_rn(D), A.r_h, A.t0, A.rh_magic);
       A.ws.chan_q0[J.chan_off + m] = q;
+      A.ws.chan_scale[J.chan_off + m] = J.normalize ? (float)D : 1.0f;  // direct path -> 1/(1 m)
       // resample.py:115-119: clip(round(q0 / r_h), 0, n2 - 1), half-even
       int di = (int)rint(__ddiv_rn((double)q, (double)A.r_h));
       A.direct_index[J.chan_off + m] = di < 0 ? 0 : (di > J.n2 - 1 ? J.n2 - 1 : di);
@@ -218,7 +221,7 @@ struct SortArgs {
   const frir_job* jobs;
   const int32_t* chan_job;
   Workspace ws;
-  int r_h, t0, e_lo, e_hi;
+  int r_h, t0;
 };
 
 constexpr int kSortThreads = 256;
@@ -244,7 +247,7 @@ __global__ void __launch_bounds__(kSortThreads) sort_kernel(SortArgs A) {
     const int sp = (v.x & 0xFFFFF) - kSpBias - kExt;
     const int phi = ((unsigned)v.x >> 20) & 0x3FF;
     const int rel = A.r_h * sp - A.t0 - phi - q0;  // q - q0
-    if (rel >= -A.e_lo && rel <= A.e_hi) v.y ^= 0x80000000;  // early: negative gain
+    if (rel >= -J.e_lo && rel <= J.e_hi) v.y ^= 0x80000000;  // early: negative gain
     s_val[r] = v;
   }
   __syncthreads();
@@ -376,24 +379,24 @@ __device__ __forceinline__ void lp_scan_tile(const float* wbuf, const double* sc
 template <bool HAS_D = true>
 __device__ __forceinline__ void store_chunk(float* out, int n_base, int n2, int nrow, int n_c,
                                             const float* dbuf, const double* s_corr, int lane,
-                                            const double (&lp)[kChunk]) {
+                                            const double (&lp)[kChunk], double scale) {
   const int n0 = n_base + kChunk * lane;
   const float4* d4 = reinterpret_cast<const float4*>(dbuf + kChunk * lane);
   float y[kChunk];
 #pragma unroll
   for (int k = 0; k < kChunk / 4; ++k) {
     const float4 v = HAS_D ? d4[k] : make_float4(0.f, 0.f, 0.f, 0.f);
-    y[4 * k] = (float)((double)v.x - lp[4 * k]);
-    y[4 * k + 1] = (float)((double)v.y - lp[4 * k + 1]);
-    y[4 * k + 2] = (float)((double)v.z - lp[4 * k + 2]);
-    y[4 * k + 3] = (float)((double)v.w - lp[4 * k + 3]);
+    y[4 * k] = (float)(((double)v.x - lp[4 * k]) * scale);  // scale == 1 unless normalising
+    y[4 * k + 1] = (float)(((double)v.y - lp[4 * k + 1]) * scale);
+    y[4 * k + 2] = (float)(((double)v.z - lp[4 * k + 2]) * scale);
+    y[4 * k + 3] = (float)(((double)v.w - lp[4 * k + 3]) * scale);
   }
   if (n0 + kChunk > n_c) {  // tail outputs: subtract the exact truncation correction
 #pragma unroll
     for (int k = 0; k < kChunk; ++k) {
       const int n = n0 + k;
       if (n >= n_c && n < n2)
-        y[k] = (float)((HAS_D ? (double)dbuf[kChunk * lane + k] : 0.0) - lp[k] - s_corr[n - n_c]);
+        y[k] = (float)(((HAS_D ? (double)dbuf[kChunk * lane + k] : 0.0) - lp[k] - s_corr[n - n_c]) * scale);
     }
   }
   if (n0 >= 0 && n0 + kChunk <= n2) {
@@ -505,8 +508,6 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(RenderArgs A)
   const Cplx v0a = {A.plan.lp[2], A.plan.lp[3]}, v0b = {A.plan.lp[4], A.plan.lp[5]};
   const int sup = d.sup, r_h = d.r_h, up = d.up, down = d.down, half1 = d.half1;
   const unsigned down_magic = (unsigned)((0x100000000ull + down - 1) / down);  // exact for e < 2^32 / down
-  const int rate = d.r_h * d.sample_rate;
-  const int e_lo = (int)(((long)6 * rate + 999) / 1000), e_hi = (int)(((long)50 * rate + 999) / 1000);
 
   for (;;) {
     int ci = 0;
@@ -520,6 +521,7 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(RenderArgs A)
     const int rows = J.n_images + 1;
     const int n1 = J.n1, n2 = J.n2;
     const int nrow = min(J.out_stride, (n2 + 3) & ~3);  // row incl. alignment padding
+    const double scale = (double)A.ws.chan_scale[c];
     const int2* items = A.ws.items + J.item_off + (size_t)m * rows;
     float* outF = A.out_full + J.out_off + (size_t)m * J.out_stride;
     float* outE = EARLY ? A.out_early + J.out_off + (size_t)m * J.out_stride : nullptr;
@@ -535,8 +537,8 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(RenderArgs A)
     int ew_lo = 0, ew_hi = -1;
     if (EARLY) {
       const int q0 = A.ws.chan_q0[c];
-      ew_lo = (ceil_div_i(q0 - e_lo + d.t0, r_h) + kExt) >> 5;
-      ew_hi = (ceil_div_i(q0 + e_hi + d.t0, r_h) + kExt + sup - 1) >> 5;
+      ew_lo = (ceil_div_i(q0 - J.e_lo + d.t0, r_h) + kExt) >> 5;
+      ew_hi = (ceil_div_i(q0 + J.e_hi + d.t0, r_h) + kExt + sup - 1) >> 5;
     }
     __syncwarp();
 
@@ -560,12 +562,12 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(RenderArgs A)
       __syncwarp();
       double lp[kChunk];
       lp_scan_tile(wF_t, s_scan, c1, c2, sF0, sF1, lane, lp);
-      store_chunk(outF, n_base, n2, nrow, n_c, dF_t, corrF_s, lane, lp);
+      store_chunk(outF, n_base, n2, nrow, n_c, dF_t, corrF_s, lane, lp, scale);
       if (EARLY) {
         const bool quiet = w0 > ew_hi;  // no early item feeds this tile: pure decay
         if (!quiet) {
           lp_scan_tile(wE_t, s_scan, c1, c2, sE0, sE1, lane, lp);
-          store_chunk(outE, n_base, n2, nrow, n_c, dE_t, corrE_s, lane, lp);
+          store_chunk(outE, n_base, n2, nrow, n_c, dE_t, corrE_s, lane, lp, scale);
         } else if (!e_dead) {
           // LP[k] = row0(M^(k+1)) . s for the whole tile; y = -LP (D = W = 0)
           const double* fr = A.plan.scan + kScanFree + 2 * kChunk * lane;  // global (L1)
@@ -575,7 +577,7 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(RenderArgs A)
           const double n0v = fma(Mt[0], sE0, Mt[1] * sE1), n1v = fma(Mt[2], sE0, Mt[3] * sE1);
           sE0 = n0v;
           sE1 = n1v;
-          store_chunk<false>(outE, n_base, n2, nrow, n_c, dE_t, corrE_s, lane, lp);
+          store_chunk<false>(outE, n_base, n2, nrow, n_c, dE_t, corrE_s, lane, lp, scale);
           e_dead = fabs(sE0) + fabs(sE1) < 1e-50;  // |LP| <= ~400 |s| < 2^-150: rounds to 0 in FP32
         } else {
           const int n0 = n_base + kChunk * lane;
@@ -803,7 +805,7 @@ int check_line() {
 }
 
 size_t workspace_bytes(const frir_batch* b) {
-  return align_up((size_t)b->total_items * 8) + align_up((size_t)b->total_channels * 4) + 256;
+  return align_up((size_t)b->total_items * 8) + 2 * align_up((size_t)b->total_channels * 4) + 256;
 }
 
 static int table_blocks(const frir_plan_desc& d) { return (d.sup + 31) / 32; }
@@ -877,8 +879,6 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_
     SortArgs sa;
     sa.jobs = b->jobs; sa.chan_job = b->chan_job; sa.ws = ws;
     sa.r_h = d.r_h; sa.t0 = d.t0;
-    sa.e_lo = (int)(((long)6 * rate + 999) / 1000);    // core.py:257
-    sa.e_hi = (int)(((long)50 * rate + 999) / 1000);   // core.py:258
     const int nbk = ((b->max_windows * kWin + kSpBias) >> 5) + 3;
     size_t smem = (size_t)b->max_rows * 8 + (size_t)nbk * kSortWarps * 2 + 16;
     e = cudaFuncSetAttribute(sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

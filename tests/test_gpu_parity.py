@@ -250,3 +250,32 @@ def test_native_statistics_match_reference_rt60():
         if np.isnan(t_ref):
             continue
         assert abs(t_gpu - t_ref) <= 0.05 * t_ref
+
+
+# ---------------------------------------------------------------- north_star extensions
+def test_extension_image_range_early_window_normalize():
+    arr = F.linear_array([0.05, 0.05])
+    scene = F.Scene(room_dims=(6.0, 5.0, 3.0), mic_positions=arr, sources=[(1.3, 0.4, 0.1), (2.1, 2.0, 0.0)])
+    # image-count range: I_k ~ U{lo..hi} from stream (seed, k, 2)
+    p = F.SimParams(t60=0.2, num_images=(300, 700), seed=21, early_window_ms=(3.0, 20.0))
+    res = F.simulate_rir(p, scene)
+    for k, r in enumerate(res):
+        u = np.random.Generator(np.random.Philox(np.random.SeedSequence((21, k, 2)))).random()
+        n_k = 300 + int(u * 401)
+        assert r.full.metadata["num_images_drawn"] == n_k
+        job = P.jobs_from_scene(F.SimParams(t60=0.2, num_images=n_k, seed=21), scene)[k]
+        full_o, early_o, _ = P.render(job, early_window_ms=(3.0, 20.0))
+        for m in range(3):
+            assert rel_err(r.full.samples[m], full_o[m]) <= TOL
+            assert rel_err(r.early.samples[m], early_o[m]) <= TOL
+    # direct-path normalisation scales channel m by its direct distance
+    base = F.simulate_rir(F.SimParams(t60=0.2, num_images=256, seed=4), scene)
+    norm = F.simulate_rir(F.SimParams(t60=0.2, num_images=256, seed=4, normalize="direct"), scene)
+    for k in range(2):
+        job = P.jobs_from_scene(F.SimParams(t60=0.2, num_images=256, seed=4), scene)[k]
+        d = P.draw(job)
+        P.delays_gains(job, d)
+        for m in range(3):
+            scale = d.mic_distances[0, m]
+            assert np.allclose(norm[k].full.samples[m], base[k].full.samples[m] * scale, rtol=1e-6, atol=1e-9)
+            assert np.allclose(norm[k].early.samples[m], base[k].early.samples[m] * scale, rtol=1e-6, atol=1e-9)
