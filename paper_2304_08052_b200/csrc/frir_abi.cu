@@ -130,7 +130,7 @@ int frir_plan_create(int32_t fs, frir_plan** out) {
   frir_plan* p = new frir_plan();
   std::string err;
   if (!design(fs, &p->design, &err)) { delete p; set_error(err); return FRIR_EINVAL; }
-  if (p->design.d.r_h > 1023 || p->design.d.sup > 64) {
+  if (p->design.d.r_h > 1023 || p->design.d.sup > 64 || p->design.d.lt_max > kLtMax) {
     delete p;
     set_error("sample_rate " + std::to_string(fs) + " is outside the supported range (r_h <= 1023, <= 64 taps)");
     return FRIR_ERANGE;

@@ -20,6 +20,10 @@ constexpr int kChunk = kTile / 32;  // serial outputs per lane in the scan
 constexpr int kExt = 32;
 constexpr int kSpBias = 64;     // bias of the packed start index
 constexpr int kMaxRows = 17408; // max images + 1 per job (K2 block sort capacity)
+constexpr int kLtMax = 128;     // max stage-1 taps past n1 (lt_max = (half1 - up) / down + 2, 91 at 11025 Hz)
+// Per-warp row length of the render kernel's past-n1 tap sums, sized per rate
+// so the 16 kHz plan keeps two CTAs per SM.
+__host__ __device__ inline int lt_cap(const frir_plan_desc& d) { return (d.lt_max + 31) & ~31; }
 
 // Device-resident, read-only per-plan data (uploaded once by frir_plan_create).
 struct DevPlan {

@@ -478,8 +478,9 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(RenderArgs A)
   float* s_tile = reinterpret_cast<float*>(s_corr_all + kWarps * V * 32);  // [warp][V][D, W][kTile]
   int2* s_items = reinterpret_cast<int2*>(s_tile + (size_t)kWarps * V * 2 * kTile);
   double4* s_zeta = reinterpret_cast<double4*>(s_items + 32 * kWarps);   // [warp][32]
-  double* s_xt = reinterpret_cast<double*>(s_zeta + 32 * kWarps);         // [warp][F, E][64]
-  float* s_head = reinterpret_cast<float*>(s_xt + 128 * kWarps);          // [warp][V][D, W][64]
+  const int ltc = lt_cap(d);                                               // xt row length
+  double* s_xt = reinterpret_cast<double*>(s_zeta + 32 * kWarps);         // [warp][F, E][ltc]
+  float* s_head = reinterpret_cast<float*>(s_xt + 2 * ltc * kWarps);      // [warp][V][D, W][64]
   double2* s_plo = reinterpret_cast<double2*>(s_head + kWarps * V * 2 * 64);  // p^i, i < 128
   double2* s_zph = s_plo + 128;                                         // Z[rho], rho < down
   double2* s_phi = s_zph + d.down;                                      // p^(128 j)
@@ -503,7 +504,7 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(RenderArgs A)
   int2* s_it = s_items + 32 * warp;
   float* head_s = s_head + warp * V * 2 * 64;
   double4* zeta_s = s_zeta + 32 * warp;
-  double* xt_s = s_xt + 128 * warp;
+  double* xt_s = s_xt + 2 * ltc * warp;
   const double c1 = A.plan.lp[0], c2 = A.plan.lp[1];
   const Cplx v0a = {A.plan.lp[2], A.plan.lp[3]}, v0b = {A.plan.lp[4], A.plan.lp[5]};
   const int sup = d.sup, r_h = d.r_h, up = d.up, down = d.down, half1 = d.half1;
@@ -531,8 +532,10 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(RenderArgs A)
     // staged (the items within the HP horizon are a suffix of the sorted list)
     const int n_c = n1 - d.half2 > 0 ? (n1 - d.half2 + d.r_l - 1) / d.r_l : 0;
     const int kthr = n1 - d.horizon;  // items with k_hi >= kthr feed the state
+    const int w_c = (n_c + kExt) >> 5;  // window of the first corrected output
+    bool tail_done = false;
     zeta_s[lane] = make_double4(0.0, 0.0, 0.0, 0.0);
-    xt_s[lane] = 0.0; xt_s[32 + lane] = 0.0; xt_s[64 + lane] = 0.0; xt_s[96 + lane] = 0.0;
+    for (int i = lane; i < 2 * ltc; i += 32) xt_s[i] = 0.0;
     // windows touched by early items (q in [q0 - lo, q0 + hi], core.py:257-264)
     int ew_lo = 0, ew_hi = -1;
     if (EARLY) {
@@ -623,14 +626,23 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(RenderArgs A)
       s_it[lane] = make_int2((int)dec, mine.y);
       __syncwarp();
       const int cnt = min(32, rows - p);
-      {  // tail: this batch's contribution to the HP state at n1
-        const int spb = mine.x & 0xFFFFF;
-        const int qm = r_h * (spb - kSpBias - kExt) - d.t0 - (((unsigned)mine.x >> 20) & 0x3FF);
+      if (!tail_done) {  // tail: contributions to the HP state at n1
+        // Finish now (scanning the remaining items too) if this batch could emit
+        // the tile holding the first corrected output, so the corrections exist
+        // before that tile is flushed; otherwise just this batch.
+        const int bk_last = __shfl_sync(0xffffffffu, bk, cnt - 1);
+        const bool finish = p + 32 >= rows || bk_last >= (w_c & ~(kTileWin - 1));
+        const int p_end = finish ? rows : p + cnt;
+        for (int pp = p; pp < p_end; pp += 32) {
+        const int2 it_t = pp == p ? mine : (pp + lane < rows ? items[pp + lane] : make_int2(0xFFFFF, 0));
+        const int cnt_t = min(32, rows - pp);
+        const int spb = it_t.x & 0xFFFFF;
+        const int qm = r_h * (spb - kSpBias - kExt) - d.t0 - (((unsigned)it_t.x >> 20) & 0x3FF);
         const int e = up * qm + half1;  // >= 0
         const int khi = (int)__umulhi((unsigned)e, down_magic);
-        const bool valid = lane < cnt && khi >= kthr;
+        const bool valid = lane < cnt_t && khi >= kthr;
         if (__any_sync(0xffffffffu, valid)) {
-          const float ae = __int_as_float(mine.y);
+          const float ae = __int_as_float(it_t.y);
           const bool early = ae < 0.f;
           const double a = fabs((double)ae);
           const bool head_item = e < 2 * half1;  // some stage-1 taps at k < 0
@@ -654,7 +666,7 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(RenderArgs A)
             const int src = __ffs(strad) - 1;
             strad &= strad - 1;
             const int qs = __shfl_sync(0xffffffffu, qm, src);
-            const float aes = __int_as_float(__shfl_sync(0xffffffffu, mine.y, src));
+            const float aes = __int_as_float(__shfl_sync(0xffffffffu, it_t.y, src));
             const double as = fabs((double)aes);
             const bool es = aes < 0.f;
             const int khs = (int)__umulhi((unsigned)(up * qs + half1), down_magic);
@@ -675,23 +687,23 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(RenderArgs A)
                 z.w = fma(cc, pm.im, z.w);
               }
             }
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {  // taps k >= n1: input past the truncation point
-              const int l = lane + 32 * h;
+            for (int l = lane; l < d.lt_max; l += 32) {  // taps k >= n1: input past the truncation point
               const int k = n1 + l;
-              if (l < d.lt_max && k <= khs) {
+              if (k <= khs) {
                 const int idx = down * k + half1 - up * qs;
                 if (idx >= 0 && idx < d.len1) {
                   const double cc = as * A.plan.h1up[idx];
                   xt_s[l] += cc;
-                  if (EARLY && es) xt_s[64 + l] += cc;
+                  if (EARLY && es) xt_s[ltc + l] += cc;
                 }
               }
             }
           }
           zeta_s[lane] = z;
         }
-        if (p + 32 >= rows) {  // every item staged: finish the state and the corrections
+        }  // chunks
+        if (finish) {  // every item accumulated: finish the state and the corrections
+          tail_done = true;
           double4 z = zeta_s[lane];
           Cplx zF = {z.x, z.y}, zE = {z.z, z.w};
 #pragma unroll
@@ -722,7 +734,7 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(RenderArgs A)
             for (int l = 0; l < d.lt_max && l <= ee; ++l) {
               const double uu = A.plan.u[ee - l];
               corrF += xt_s[l] * uu;
-              if (EARLY) corrE += xt_s[64 + l] * uu;
+              if (EARLY) corrE += xt_s[ltc + l] * uu;
             }
           }
           corrF_s[lane] = corrF;
@@ -815,7 +827,7 @@ static size_t render_smem(const frir_plan_desc& d, bool early) {
   return (size_t)d.r_h * 64 * table_blocks(d) * 8 + kScanSmem * 8 + (size_t)kWarps * v * 32 * 8 +
          (size_t)kWarps * v * 2 * kTile * 4 + (size_t)kWarps * 32 * 8 +
          (size_t)kWarps * v * 2 * 64 * 4 + (size_t)(128 + d.down + d.horizon / 128 + 1) * 16 +
-         (size_t)kWarps * (32 * 32 + 128 * 8);
+         (size_t)kWarps * (32 * 32 + 2 * lt_cap(d) * 8);
 }
 
 template <bool EARLY, int NBK>

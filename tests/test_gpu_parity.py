@@ -279,3 +279,49 @@ def test_extension_image_range_early_window_normalize():
             scale = d.mic_distances[0, m]
             assert np.allclose(norm[k].full.samples[m], base[k].full.samples[m] * scale, rtol=1e-6, atol=1e-9)
             assert np.allclose(norm[k].early.samples[m], base[k].early.samples[m] * scale, rtol=1e-6, atol=1e-9)
+
+
+# ---------------------------------------------------------------- randomized scenes
+def _random_job(rng):
+    fs = int(rng.choice([8000, 11025, 16000, 22050, 24000, 32000, 44100, 48000]))
+    t60 = float(rng.uniform(0.05, 0.35))
+    m = int(rng.integers(1, 6))
+    room = rng.uniform([3.0, 3.0, 2.4], [9.0, 9.0, 4.0])
+    mics = rng.uniform(-0.12, 0.12, size=(m, 3))
+    center = mics.mean(axis=0)
+    r = P.wall_reflection(room, t60)
+    d_min = max(0.02, 343.0 * t60 / (1000.0 * r) * 1.05)  # keeps RR_max >= 1
+    d0 = float(rng.uniform(d_min, d_min + 2.5))
+    n = int(rng.choice([0, 1, 7, 64, 333, 1024, 2500]))
+    return P.Job(room=tuple(room), mics=mics, center=center,
+                 source=(d0, float(rng.uniform(0, 2 * np.pi)), float(rng.uniform(-1.2, 1.2))),
+                 t60=t60, sample_rate=fs, num_images=n, seed=int(rng.integers(2**63)),
+                 source_index=int(rng.integers(0, 3)))
+
+
+@pytest.mark.parametrize("seed", range(32))
+def test_random_scenes_match_oracle(seed):
+    """Random rates, T60s, image counts, mic layouts (incl. mics near the
+    source) and seeds: the CUDA path equals the oracle within 1e-5 of peak."""
+    rng = np.random.default_rng(1000 + seed)
+    job = _random_job(rng)
+    try:
+        full_o, early_o, direct_o = P.render(job)
+    except ValueError:
+        pytest.skip("scene rejected by the reference rules")
+    jobs = engine.new_jobs(1)
+    jobs["room"] = job.room
+    jobs["center"] = job.center
+    jobs["d0"], jobs["az"], jobs["el"] = job.source
+    jobs["t60"] = job.t60
+    jobs["seed"] = job.seed
+    jobs["source_index"] = job.source_index
+    jobs["n_images"] = job.num_images
+    jobs["n_mics"] = len(job.mics)
+    res = engine.simulate_jobs(job.sample_rate, jobs, job.mics, include_early=True)
+    full, early = res.job_view(0).cpu().numpy(), res.job_view(0, "early").cpu().numpy()
+    assert np.isfinite(full).all() and np.isfinite(early).all()
+    for m in range(len(job.mics)):
+        assert rel_err(full[m], full_o[m]) <= TOL, (seed, job.sample_rate, m)
+        assert rel_err(early[m], early_o[m]) <= TOL, (seed, job.sample_rate, m)
+    assert np.array_equal(res.direct_index.cpu().numpy(), direct_o)
