@@ -477,14 +477,13 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(RenderArgs A)
   double* s_corr_all = s_scan + kScanSmem;                                 // [warp][V][32]
   float* s_tile = reinterpret_cast<float*>(s_corr_all + kWarps * V * 32);  // [warp][V][D, W][kTile]
   int2* s_items = reinterpret_cast<int2*>(s_tile + (size_t)kWarps * V * 2 * kTile);
-  double4* s_zeta = reinterpret_cast<double4*>(s_items + 32 * kWarps);   // [warp][32]
-  const int ltc = lt_cap(d);                                               // xt row length
-  double* s_xt = reinterpret_cast<double*>(s_zeta + 32 * kWarps);         // [warp][F, E][ltc]
-  float* s_head = reinterpret_cast<float*>(s_xt + 2 * ltc * kWarps);      // [warp][V][D, W][64]
+  float* s_head = reinterpret_cast<float*>(s_items + 32 * kWarps);          // [warp][V][D, W][64]
   double2* s_plo = reinterpret_cast<double2*>(s_head + kWarps * V * 2 * 64);  // p^i, i < 128
   double2* s_zph = s_plo + 128;                                         // Z[rho], rho < down
   double2* s_phi = s_zph + d.down;                                      // p^(128 j)
   const int nphi = d.horizon / 128 + 1;
+  const int ltc = lt_cap(d);                                 // xt row length (last: per-rate size)
+  double* s_xt = reinterpret_cast<double*>(s_phi + nphi);   // [warp][F, E][ltc]
   for (int i = threadIdx.x; i < ncomp; i += blockDim.x) s_comp[i] = A.plan.comp[i];
   for (int i = threadIdx.x; i < 128; i += blockDim.x) s_plo[i] = make_double2(A.plan.ppow_lo[2 * i], A.plan.ppow_lo[2 * i + 1]);
   for (int i = threadIdx.x; i < d.down; i += blockDim.x) s_zph[i] = make_double2(A.plan.zphase[2 * i], A.plan.zphase[2 * i + 1]);
@@ -503,7 +502,6 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(RenderArgs A)
   double* corrE_s = corrF_s + 32;
   int2* s_it = s_items + 32 * warp;
   float* head_s = s_head + warp * V * 2 * 64;
-  double4* zeta_s = s_zeta + 32 * warp;
   double* xt_s = s_xt + 2 * ltc * warp;
   const double c1 = A.plan.lp[0], c2 = A.plan.lp[1];
   const Cplx v0a = {A.plan.lp[2], A.plan.lp[3]}, v0b = {A.plan.lp[4], A.plan.lp[5]};
@@ -528,13 +526,10 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(RenderArgs A)
     float* outE = EARLY ? A.out_early + J.out_off + (size_t)m * J.out_stride : nullptr;
 
     // ---- tail state (truncation at n1, resample.py:107-113): per-lane partial
-    // modal sums and the taps past n1 accumulate in smem while the items are
-    // staged (the items within the HP horizon are a suffix of the sorted list)
+    // modal sums and the taps past n1, accumulated in smem by a pre-pass over
+    // the items within the HP horizon (a suffix of the bucket-sorted list)
     const int n_c = n1 - d.half2 > 0 ? (n1 - d.half2 + d.r_l - 1) / d.r_l : 0;
     const int kthr = n1 - d.horizon;  // items with k_hi >= kthr feed the state
-    const int w_c = (n_c + kExt) >> 5;  // window of the first corrected output
-    bool tail_done = false;
-    zeta_s[lane] = make_double4(0.0, 0.0, 0.0, 0.0);
     for (int i = lane; i < 2 * ltc; i += 32) xt_s[i] = 0.0;
     // windows touched by early items (q in [q0 - lo, q0 + hi], core.py:257-264)
     int ew_lo = 0, ew_hi = -1;
@@ -545,11 +540,185 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(RenderArgs A)
     }
     __syncwarp();
 
+    // ---- head pre-pass: items whose stage-1 taps reach mid index < 0 (a
+    // prefix of the bucket-sorted list; only sources within a few cm of a mic)
+    bool head_on = false;  // head corrections pending in head_s
+    for (int p = 0; p < rows; p += 32) {
+      const int2 mine = p + lane < rows ? items[p + lane] : make_int2(0xFFFFF, 0);
+      const int cnt = min(32, rows - p);
+      const int qm = r_h * ((mine.x & 0xFFFFF) - kSpBias - kExt) - d.t0 - (((unsigned)mine.x >> 20) & 0x3FF);
+      unsigned hm = __ballot_sync(0xffffffffu, lane < cnt && up * qm < half1);
+      if (hm) {
+        if (!head_on) {
+          for (int i = lane; i < V * 2 * 64; i += 32) head_s[i] = 0.f;
+          head_on = true;
+        }
+        while (hm) {
+          const int src = __ffs(hm) - 1;
+          hm &= hm - 1;
+          const int qs = __shfl_sync(0xffffffffu, qm, src);
+          const float aes = __int_as_float(__shfl_sync(0xffffffffu, mine.y, src));
+          const double as = fabs((double)aes);
+          const int xs = up * qs - half1 + 1024 * down;
+          const int klo = (int)__umulhi((unsigned)xs, down_magic) - 1024 + (xs % down != 0);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int np = lane + 32 * h;  // n'' in [0, 64)
+            const int n = np - kExt;
+            double cd = 0.0, cw = 0.0;
+            for (int k = klo; k < 0; ++k) {
+              FRIR_CHECK(down * k + half1 - up * qs >= 0 && down * k + half1 - up * qs < d.len1);
+              const double cc = as * A.plan.h1up[down * k + half1 - up * qs];
+              const int idx = d.r_l * n + d.half2 - k;
+              if (idx >= 0 && idx < d.len2) cd += cc * A.plan.h2[idx];
+              if (idx >= 0 && idx < d.len2 + 2 * d.r_l) cw += cc * A.plan.gw[idx];
+            }
+            head_s[np] -= (float)cd;
+            head_s[64 + np] -= (float)cw;
+            if (EARLY && aes < 0.f) {
+              head_s[128 + np] -= (float)cd;
+              head_s[192 + np] -= (float)cw;
+            }
+          }
+        }
+        __syncwarp();
+      }
+      // later items have bucket >= this batch's last: stop once none can be a head item
+      const int bk_last = __shfl_sync(0xffffffffu, (mine.x & 0xFFFFF) >> 5, cnt - 1);
+      const long long qmin = (long long)r_h * ((bk_last << 5) - kSpBias - kExt) - d.t0 - (r_h - 1);
+      if ((long long)up * qmin >= half1) break;
+    }
+
+    // ---- tail pre-pass: find the suffix whose k_hi can reach kthr (earlier
+    // items have bucket <= a batch's first bucket, bounding their k_hi), then
+    // accumulate it and finish the boundary state and the corrections
+    int p_t = 0;
+    if (kthr > 0) {
+      const int nb = (rows + 31) >> 5;
+      p_t = -1;
+      for (int b0 = nb - 1; b0 >= 0 && p_t < 0; b0 -= 32) {  // 32 batch starts per round
+        const int b = b0 - lane;
+        bool below = true;  // every item before batch b has k_hi < kthr
+        if (b > 0) {
+          const int bkf = (items[32 * b].x & 0xFFFFF) >> 5;
+          const long long qmax = (long long)r_h * ((bkf << 5) + 31 - kSpBias - kExt) - d.t0;
+          below = (long long)up * qmax + half1 < (long long)kthr * down;
+        }
+        const unsigned bm = __ballot_sync(0xffffffffu, b >= 0 && below);
+        if (bm) p_t = 32 * (b0 - (__ffs(bm) - 1));
+      }
+      p_t = max(p_t, 0);
+    }
+    double4 z = make_double4(0.0, 0.0, 0.0, 0.0);  // this lane's partial modal sums (F, E)
+    for (int p = p_t; p < rows; p += 32) {
+      const int2 it_t = p + lane < rows ? items[p + lane] : make_int2(0xFFFFF, 0);
+      const int cnt_t = min(32, rows - p);
+      const int spb = it_t.x & 0xFFFFF;
+      const int qm = r_h * (spb - kSpBias - kExt) - d.t0 - (((unsigned)it_t.x >> 20) & 0x3FF);
+      const int e = up * qm + half1;  // >= 0
+      const int khi = (int)__umulhi((unsigned)e, down_magic);
+      const bool valid = lane < cnt_t && khi >= kthr;
+      if (__any_sync(0xffffffffu, valid)) {
+        const float ae = __int_as_float(it_t.y);
+        const bool early = ae < 0.f;
+        const double a = fabs((double)ae);
+        const bool head_item = e < 2 * half1;  // some stage-1 taps at k < 0
+        if (valid && khi < n1 && !head_item) {
+          const int rho = e - down * khi;
+          const int mm = n1 - 1 - khi;
+          FRIR_CHECK(mm >= 0 && (mm >> 7) < nphi && rho >= 0 && rho < down);
+          const double2 lo = s_plo[mm & 127], hi = s_phi[mm >> 7], zr = s_zph[rho];
+          const Cplx t = cmul(cmul({hi.x, hi.y}, {lo.x, lo.y}), {zr.x, zr.y});
+          z.x = fma(a, t.re, z.x);
+          z.y = fma(a, t.im, z.y);
+          if (EARLY && early) {
+            z.z = fma(a, t.re, z.z);
+            z.w = fma(a, t.im, z.w);
+          }
+        }
+        // straddlers (taps on both sides of n1) and head items: one at a time
+        unsigned strad = __ballot_sync(0xffffffffu, valid && (khi >= n1 || head_item));
+        while (strad) {
+          const int src = __ffs(strad) - 1;
+          strad &= strad - 1;
+          const int qs = __shfl_sync(0xffffffffu, qm, src);
+          const float aes = __int_as_float(__shfl_sync(0xffffffffu, it_t.y, src));
+          const double as = fabs((double)aes);
+          const bool es = aes < 0.f;
+          const int khs = (int)__umulhi((unsigned)(up * qs + half1), down_magic);
+          const int xs = up * qs - half1 + 1024 * down;  // >= 0 (half1 = 10 r_h <= 1024 down)
+          const int klo = max(0, (int)__umulhi((unsigned)xs, down_magic) - 1024 + (xs % down != 0));
+          const int kend = min(khs + 1, n1);
+          for (int k = klo + lane; k < kend; k += 32) {  // taps 0 <= k < n1 feed the state
+            const int mm = n1 - 1 - k;
+            if (mm >= d.horizon) continue;
+            FRIR_CHECK(down * k + half1 - up * qs >= 0 && down * k + half1 - up * qs < d.len1);
+            const double cc = as * A.plan.h1up[down * k + half1 - up * qs];
+            const double2 lo = s_plo[mm & 127], hi = s_phi[mm >> 7];
+            const Cplx pm = cmul({hi.x, hi.y}, {lo.x, lo.y});
+            z.x = fma(cc, pm.re, z.x);
+            z.y = fma(cc, pm.im, z.y);
+            if (EARLY && es) {
+              z.z = fma(cc, pm.re, z.z);
+              z.w = fma(cc, pm.im, z.w);
+            }
+          }
+          for (int l = lane; l < d.lt_max; l += 32) {  // taps k >= n1: input past the truncation point
+            const int k = n1 + l;
+            if (k <= khs) {
+              const int idx = down * k + half1 - up * qs;
+              if (idx >= 0 && idx < d.len1) {
+                const double cc = as * A.plan.h1up[idx];
+                xt_s[l] += cc;
+                if (EARLY && es) xt_s[ltc + l] += cc;
+              }
+            }
+          }
+        }
+      }
+    }
+    {  // boundary state s = 2 Re(v0 zeta) and the corrections of outputs n >= n_c
+      Cplx zF = {z.x, z.y}, zE = {z.z, z.w};
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        zF.re += __shfl_xor_sync(0xffffffffu, zF.re, o);
+        zF.im += __shfl_xor_sync(0xffffffffu, zF.im, o);
+        if (EARLY) {
+          zE.re += __shfl_xor_sync(0xffffffffu, zE.re, o);
+          zE.im += __shfl_xor_sync(0xffffffffu, zE.im, o);
+        }
+    }
+    __syncwarp();
+    double corrF = 0.0, corrE = 0.0;
+    const Cplx ta = cmul(v0a, zF), tb = cmul(v0b, zF);  // s = 2 Re(v0 zeta)
+    const double s0 = 2.0 * ta.re, s1 = 2.0 * tb.re;
+    double se0 = 0.0, se1 = 0.0;
+    if (EARLY) {
+      const Cplx ea = cmul(v0a, zE), eb = cmul(v0b, zE);
+      se0 = 2.0 * ea.re;
+      se1 = 2.0 * eb.re;
+    }
+    const int n = n_c + lane;
+    const int ee = d.r_l * n + d.half2 - n1;
+    const bool act = n < n2 && ee >= 0 && ee < d.half2;
+    if (act) {
+      corrF = A.plan.kappa[2 * ee] * s0 + A.plan.kappa[2 * ee + 1] * s1;
+      if (EARLY) corrE = A.plan.kappa[2 * ee] * se0 + A.plan.kappa[2 * ee + 1] * se1;
+      for (int l = 0; l < d.lt_max && l <= ee; ++l) {
+        const double uu = A.plan.u[ee - l];
+        corrF += xt_s[l] * uu;
+        if (EARLY) corrE += xt_s[ltc + l] * uu;
+      }
+    }
+    corrF_s[lane] = corrF;
+    if (EARLY) corrE_s[lane] = corrE;
+    __syncwarp();
+    }
+
     // ---- ordered sweep: windows w = -2 .. nwin-1 over n'' = n + kExt
     const int nwin = (n2 + kExt + kWin - 1) / kWin;
     Channel<EARLY, NBK> ch;
     ch.clear();
-    bool head_on = false;  // head corrections pending in head_s
     double sF0 = 0.0, sF1 = 0.0, sE0 = 0.0, sE1 = 0.0;
     bool e_dead = false;  // early state below FP32 resolution: outputs are exact zeros
     int w = -2;           // window held by the front accumulators
@@ -626,161 +795,6 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(RenderArgs A)
       s_it[lane] = make_int2((int)dec, mine.y);
       __syncwarp();
       const int cnt = min(32, rows - p);
-      if (!tail_done) {  // tail: contributions to the HP state at n1
-        // Finish now (scanning the remaining items too) if this batch could emit
-        // the tile holding the first corrected output, so the corrections exist
-        // before that tile is flushed; otherwise just this batch.
-        const int bk_last = __shfl_sync(0xffffffffu, bk, cnt - 1);
-        const bool finish = p + 32 >= rows || bk_last >= (w_c & ~(kTileWin - 1));
-        const int p_end = finish ? rows : p + cnt;
-        for (int pp = p; pp < p_end; pp += 32) {
-        const int2 it_t = pp == p ? mine : (pp + lane < rows ? items[pp + lane] : make_int2(0xFFFFF, 0));
-        const int cnt_t = min(32, rows - pp);
-        const int spb = it_t.x & 0xFFFFF;
-        const int qm = r_h * (spb - kSpBias - kExt) - d.t0 - (((unsigned)it_t.x >> 20) & 0x3FF);
-        const int e = up * qm + half1;  // >= 0
-        const int khi = (int)__umulhi((unsigned)e, down_magic);
-        const bool valid = lane < cnt_t && khi >= kthr;
-        if (__any_sync(0xffffffffu, valid)) {
-          const float ae = __int_as_float(it_t.y);
-          const bool early = ae < 0.f;
-          const double a = fabs((double)ae);
-          const bool head_item = e < 2 * half1;  // some stage-1 taps at k < 0
-          double4 z = zeta_s[lane];
-          if (valid && khi < n1 && !head_item) {
-            const int rho = e - down * khi;
-            const int mm = n1 - 1 - khi;
-            FRIR_CHECK(mm >= 0 && (mm >> 7) < nphi && rho >= 0 && rho < down);
-            const double2 lo = s_plo[mm & 127], hi = s_phi[mm >> 7], zr = s_zph[rho];
-            const Cplx t = cmul(cmul({hi.x, hi.y}, {lo.x, lo.y}), {zr.x, zr.y});
-            z.x = fma(a, t.re, z.x);
-            z.y = fma(a, t.im, z.y);
-            if (EARLY && early) {
-              z.z = fma(a, t.re, z.z);
-              z.w = fma(a, t.im, z.w);
-            }
-          }
-          // straddlers (taps on both sides of n1) and head items: one at a time
-          unsigned strad = __ballot_sync(0xffffffffu, valid && (khi >= n1 || head_item));
-          while (strad) {
-            const int src = __ffs(strad) - 1;
-            strad &= strad - 1;
-            const int qs = __shfl_sync(0xffffffffu, qm, src);
-            const float aes = __int_as_float(__shfl_sync(0xffffffffu, it_t.y, src));
-            const double as = fabs((double)aes);
-            const bool es = aes < 0.f;
-            const int khs = (int)__umulhi((unsigned)(up * qs + half1), down_magic);
-            const int xs = up * qs - half1 + 1024 * down;  // >= 0 (half1 = 10 r_h <= 1024 down)
-            const int klo = max(0, (int)__umulhi((unsigned)xs, down_magic) - 1024 + (xs % down != 0));
-            const int kend = min(khs + 1, n1);
-            for (int k = klo + lane; k < kend; k += 32) {  // taps 0 <= k < n1 feed the state
-              const int mm = n1 - 1 - k;
-              if (mm >= d.horizon) continue;
-              FRIR_CHECK(down * k + half1 - up * qs >= 0 && down * k + half1 - up * qs < d.len1);
-              const double cc = as * A.plan.h1up[down * k + half1 - up * qs];
-              const double2 lo = s_plo[mm & 127], hi = s_phi[mm >> 7];
-              const Cplx pm = cmul({hi.x, hi.y}, {lo.x, lo.y});
-              z.x = fma(cc, pm.re, z.x);
-              z.y = fma(cc, pm.im, z.y);
-              if (EARLY && es) {
-                z.z = fma(cc, pm.re, z.z);
-                z.w = fma(cc, pm.im, z.w);
-              }
-            }
-            for (int l = lane; l < d.lt_max; l += 32) {  // taps k >= n1: input past the truncation point
-              const int k = n1 + l;
-              if (k <= khs) {
-                const int idx = down * k + half1 - up * qs;
-                if (idx >= 0 && idx < d.len1) {
-                  const double cc = as * A.plan.h1up[idx];
-                  xt_s[l] += cc;
-                  if (EARLY && es) xt_s[ltc + l] += cc;
-                }
-              }
-            }
-          }
-          zeta_s[lane] = z;
-        }
-        }  // chunks
-        if (finish) {  // every item accumulated: finish the state and the corrections
-          tail_done = true;
-          double4 z = zeta_s[lane];
-          Cplx zF = {z.x, z.y}, zE = {z.z, z.w};
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            zF.re += __shfl_xor_sync(0xffffffffu, zF.re, o);
-            zF.im += __shfl_xor_sync(0xffffffffu, zF.im, o);
-            if (EARLY) {
-              zE.re += __shfl_xor_sync(0xffffffffu, zE.re, o);
-              zE.im += __shfl_xor_sync(0xffffffffu, zE.im, o);
-            }
-          }
-          __syncwarp();
-          double corrF = 0.0, corrE = 0.0;
-          const Cplx ta = cmul(v0a, zF), tb = cmul(v0b, zF);  // s = 2 Re(v0 zeta)
-          const double s0 = 2.0 * ta.re, s1 = 2.0 * tb.re;
-          double se0 = 0.0, se1 = 0.0;
-          if (EARLY) {
-            const Cplx ea = cmul(v0a, zE), eb = cmul(v0b, zE);
-            se0 = 2.0 * ea.re;
-            se1 = 2.0 * eb.re;
-          }
-          const int n = n_c + lane;
-          const int ee = d.r_l * n + d.half2 - n1;
-          const bool act = n < n2 && ee >= 0 && ee < d.half2;
-          if (act) {
-            corrF = A.plan.kappa[2 * ee] * s0 + A.plan.kappa[2 * ee + 1] * s1;
-            if (EARLY) corrE = A.plan.kappa[2 * ee] * se0 + A.plan.kappa[2 * ee + 1] * se1;
-            for (int l = 0; l < d.lt_max && l <= ee; ++l) {
-              const double uu = A.plan.u[ee - l];
-              corrF += xt_s[l] * uu;
-              if (EARLY) corrE += xt_s[ltc + l] * uu;
-            }
-          }
-          corrF_s[lane] = corrF;
-          if (EARLY) corrE_s[lane] = corrE;
-          __syncwarp();
-        }
-      }
-      {  // head: stage-1 taps at mid index < 0 do not exist in the reference (resample.py:107)
-        const int qm = r_h * ((mine.x & 0xFFFFF) - kSpBias - kExt) - d.t0 - (((unsigned)mine.x >> 20) & 0x3FF);
-        unsigned hm = __ballot_sync(0xffffffffu, lane < cnt && up * qm < half1);
-        if (hm) {
-          if (!head_on) {
-            for (int i = lane; i < V * 2 * 64; i += 32) head_s[i] = 0.f;
-            head_on = true;
-          }
-          while (hm) {
-            const int src = __ffs(hm) - 1;
-            hm &= hm - 1;
-            const int qs = __shfl_sync(0xffffffffu, qm, src);
-            const float aes = __int_as_float(__shfl_sync(0xffffffffu, mine.y, src));
-            const double as = fabs((double)aes);
-            const int xs = up * qs - half1 + 1024 * down;
-            const int klo = (int)__umulhi((unsigned)xs, down_magic) - 1024 + (xs % down != 0);
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int np = lane + 32 * h;  // n'' in [0, 64)
-              const int n = np - kExt;
-              double cd = 0.0, cw = 0.0;
-              for (int k = klo; k < 0; ++k) {
-                FRIR_CHECK(down * k + half1 - up * qs >= 0 && down * k + half1 - up * qs < d.len1);
-                const double cc = as * A.plan.h1up[down * k + half1 - up * qs];
-                const int idx = d.r_l * n + d.half2 - k;
-                if (idx >= 0 && idx < d.len2) cd += cc * A.plan.h2[idx];
-                if (idx >= 0 && idx < d.len2 + 2 * d.r_l) cw += cc * A.plan.gw[idx];
-              }
-              head_s[np] -= (float)cd;
-              head_s[64 + np] -= (float)cw;
-              if (EARLY && aes < 0.f) {
-                head_s[128 + np] -= (float)cd;
-                head_s[192 + np] -= (float)cw;
-              }
-            }
-          }
-          __syncwarp();
-        }
-      }
       const unsigned emask = EARLY ? __ballot_sync(0xffffffffu, lane < cnt && mine.y < 0) : 0u;
       int jj = 0;
       while (jj < cnt) {  // runs of equal bucket (items are bucket-sorted)
@@ -827,7 +841,7 @@ static size_t render_smem(const frir_plan_desc& d, bool early) {
   return (size_t)d.r_h * 64 * table_blocks(d) * 8 + kScanSmem * 8 + (size_t)kWarps * v * 32 * 8 +
          (size_t)kWarps * v * 2 * kTile * 4 + (size_t)kWarps * 32 * 8 +
          (size_t)kWarps * v * 2 * 64 * 4 + (size_t)(128 + d.down + d.horizon / 128 + 1) * 16 +
-         (size_t)kWarps * (32 * 32 + 2 * lt_cap(d) * 8);
+         (size_t)kWarps * 2 * lt_cap(d) * 8;
 }
 
 template <bool EARLY, int NBK>
