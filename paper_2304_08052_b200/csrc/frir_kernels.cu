@@ -4,16 +4,14 @@
 //                     FP64 image position, r^g, then per mic the exact integer
 //                     delay q, FP32 gain and output-rate start/phase items
 //                                                             core.py:131-251
-//   K2 sort_kernel    per channel: early flags, stable counting sort of the
-//                     items by 32-sample output window        core.py:254-265
+//   K2 sort_kernel    per channel: early flags, stable two-pass counting sort
+//                     of the items by 32-sample output window core.py:254-265
 //   K3 render_kernel  persistent warps, one channel at a time: gather the
 //                     composite decimation/low-pass tables into 32-sample
 //                     windows (FP32), FP64 output-rate LP scan, exact tail
 //                     correction, coalesced full + early stores
 //                                                             resample.py:81-136
 // No atomics touch sample values, so outputs are bit-reproducible.
-#include <cub/block/block_radix_sort.cuh>
-
 #include "frir_internal.h"
 #include "frir_philox.cuh"
 
@@ -39,7 +37,8 @@ constexpr double kHalfPi = 1.5707963267948966;     // np.pi / 2.0
 constexpr double kPi = 3.141592653589793;          // np.pi/2 - (-np.pi/2)
 
 struct Workspace {
-  int2* items;
+  int2* items;      // per channel, sorted by output window (K2 -> K3)
+  int2* items_raw;  // per channel, image order (K1 -> K2)
   int* chan_q0;
   float* chan_scale;
   int* counter;
@@ -51,6 +50,7 @@ Workspace carve(void* base, const frir_batch* b) {
   char* p = (char*)base;
   Workspace w;
   w.items = (int2*)p; p += align_up((size_t)b->total_items * 8);
+  w.items_raw = (int2*)p; p += align_up((size_t)b->total_items * 8);
   w.chan_q0 = (int*)p; p += align_up((size_t)b->total_channels * 4);
   w.chan_scale = (float*)p; p += align_up((size_t)b->total_channels * 4);
   w.counter = (int*)p;
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(128) geom_kernel(GeomArgs A) {
   const int ngroups = (I + 3) / 4;
   const double* mics = A.mics + 3 * (size_t)J.mic_off;
   const double rate_c0 = __ddiv_rn(A.rate, J.c0);
-  int2* items = A.ws.items + J.item_off;
+  int2* items = A.ws.items_raw + J.item_off;
   if (g == 0) {  // row 0: direct path (core.py:169, params.py:156-159), r**0 = 1
     double x, y, z;
     image_position(J, J.d0, J.az, J.el, &x, &y, &z);
@@ -227,74 +227,89 @@ struct SortArgs {
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
 
+// Two passes over the channel's raw items (K1's output, read twice; the second
+// read hits L2): per-warp 16-bit bucket histograms over contiguous row chunks,
+// one exclusive scan in (bucket, warp) order, then a stable scatter into the
+// sorted buffer.  Only the counters live in smem, so long channels keep the
+// SM occupied.
 __global__ void __launch_bounds__(kSortThreads) sort_kernel(SortArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_wsum[kSortWarps];
   const int c = blockIdx.x;
   const int j = A.chan_job[c];
   const frir_job& J = A.jobs[j];
   const int m = c - J.chan_off;
   const int rows = J.n_images + 1;
   const int nbk = ((J.n2 + kExt + kSpBias) >> 5) + 2;  // buckets 0 .. nbk-1
-  int2* items = A.ws.items + J.item_off + (size_t)m * rows;
-  int2* s_val = reinterpret_cast<int2*>(smem);
-  unsigned short* s_cnt = reinterpret_cast<unsigned short*>(s_val + rows);  // [nbk][warps]
-  __shared__ int s_part[kSortThreads];
+  const size_t base = J.item_off + (size_t)m * rows;
+  const int2* src = A.ws.items_raw + base;
+  int2* dst = A.ws.items + base;
+  unsigned short* s_cnt = reinterpret_cast<unsigned short*>(smem);  // [nbk][warps]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int q0 = A.ws.chan_q0[c];
-  for (int i = tid; i < nbk * kSortWarps; i += kSortThreads) s_cnt[i] = 0;
-  for (int r = tid; r < rows; r += kSortThreads) {
-    int2 v = items[r];
-    const int sp = (v.x & 0xFFFFF) - kSpBias - kExt;
-    const int phi = ((unsigned)v.x >> 20) & 0x3FF;
-    const int rel = A.r_h * sp - A.t0 - phi - q0;  // q - q0
-    if (rel >= -J.e_lo && rel <= J.e_hi) v.y ^= 0x80000000;  // early: negative gain
-    s_val[r] = v;
-  }
+  const int n = nbk * kSortWarps;
+  for (int i = tid; i < (n + 1) / 2; i += kSortThreads) reinterpret_cast<unsigned*>(s_cnt)[i] = 0u;
   __syncthreads();
-  // per-warp histograms over a contiguous row chunk per warp
+  // pass 1: per-warp histograms over a contiguous row chunk per warp
   const int chunk = (rows + kSortWarps - 1) / kSortWarps;
   const int r_lo = warp * chunk, r_hi = min(rows, r_lo + chunk);
+#pragma unroll 4
   for (int r = r_lo + lane; r < r_hi; r += 32) {
-    const int b = (s_val[r].x & 0xFFFFF) >> 5;
+    const int b = (__ldg(&src[r].x) & 0xFFFFF) >> 5;
     atomicAdd(reinterpret_cast<unsigned*>(s_cnt) + ((b * kSortWarps + warp) >> 1),
               1u << (16 * ((b * kSortWarps + warp) & 1)));
   }
   __syncthreads();
-  // exclusive scan over (bucket, warp) in bucket-major order
-  const int n = nbk * kSortWarps;
+  // exclusive scan over (bucket, warp) in bucket-major order: serial per
+  // thread, shuffles within a warp, one smem round across warps
   const int per = (n + kSortThreads - 1) / kSortThreads;
   const int lo = tid * per, hi = min(n, lo + per);
   int sum = 0;
   for (int i = lo; i < hi; ++i) sum += s_cnt[i];
-  s_part[tid] = sum;
-  __syncthreads();
-  for (int off = 1; off < kSortThreads; off <<= 1) {
-    int v = tid >= off ? s_part[tid - off] : 0;
-    __syncthreads();
-    s_part[tid] += v;
-    __syncthreads();
+  int inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
   }
-  int run = s_part[tid] - sum;
+  if (lane == 31) s_wsum[warp] = inc;
+  __syncthreads();
+  int run = inc - sum;
+  for (int w2 = 0; w2 < warp; ++w2) run += s_wsum[w2];
   for (int i = lo; i < hi; ++i) {
-    int cnt = s_cnt[i];
+    const int cnt = s_cnt[i];
     s_cnt[i] = (unsigned short)run;
     run += cnt;
   }
   __syncthreads();
-  // stable scatter: warp w walks its chunk in row order
-  for (int base = r_lo; base < r_hi; base += 32) {
-    const int r = base + lane;
+  // pass 2: stable scatter, warp w walks its chunk in row order; early flags
+  // (core.py:259-264) from the channel's direct arrival q0
+  const int q0 = A.ws.chan_q0[c];
+  const int kbits = 32 - __clz(nbk + 31);  // bits of every key below nbk + 32
+  int2 v = r_lo + lane < r_hi ? src[r_lo + lane] : make_int2(0, 0);
+  for (int rb = r_lo; rb < r_hi; rb += 32) {
+    const int r = rb + lane;
     const bool ok = r < r_hi;
-    int2 v = ok ? s_val[r] : make_int2(0, 0);
-    const int b = ok ? (v.x & 0xFFFFF) >> 5 : -1 - lane;
-    const unsigned peers = __match_any_sync(0xffffffffu, b);
+    const int2 cur = v;
+    if (r + 32 < r_hi) v = src[r + 32];  // prefetch the next row group
+    int2 it = cur;
+    const int sp = (it.x & 0xFFFFF) - kSpBias - kExt;
+    const int phi = ((unsigned)it.x >> 20) & 0x3FF;
+    const int rel = A.r_h * sp - A.t0 - phi - q0;  // q - q0
+    if (rel >= -J.e_lo && rel <= J.e_hi) it.y ^= 0x80000000;  // early: negative gain
+    const int b = ok ? (it.x & 0xFFFFF) >> 5 : nbk + lane;  // distinct for idle lanes
+    unsigned peers = 0xffffffffu;  // lanes with the same bucket: one ballot per key bit
+    for (int k = 0; k < kbits; ++k) {
+      const bool bit = (b >> k) & 1;
+      const unsigned ones = __ballot_sync(0xffffffffu, bit);
+      peers &= bit ? ones : ~ones;
+    }
     const int rank = __popc(peers & ((1u << lane) - 1u));
     unsigned short* slot = s_cnt + (ok ? b * kSortWarps + warp : 0);
     const int pos = ok ? *slot + rank : 0;
     FRIR_CHECK(!ok || (pos >= 0 && pos < rows && b < nbk));
     __syncwarp();
     if (ok) {
-      items[pos] = v;
+      dst[pos] = it;
       if (rank == 0) *slot = (unsigned short)(*slot + __popc(peers));
     }
     __syncwarp();
@@ -831,7 +846,7 @@ int check_line() {
 }
 
 size_t workspace_bytes(const frir_batch* b) {
-  return align_up((size_t)b->total_items * 8) + 2 * align_up((size_t)b->total_channels * 4) + 256;
+  return 2 * align_up((size_t)b->total_items * 8) + 2 * align_up((size_t)b->total_channels * 4) + 256;
 }
 
 static int table_blocks(const frir_plan_desc& d) { return (d.sup + 31) / 32; }
@@ -906,7 +921,7 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_
     sa.jobs = b->jobs; sa.chan_job = b->chan_job; sa.ws = ws;
     sa.r_h = d.r_h; sa.t0 = d.t0;
     const int nbk = ((b->max_windows * kWin + kSpBias) >> 5) + 3;
-    size_t smem = (size_t)b->max_rows * 8 + (size_t)nbk * kSortWarps * 2 + 16;
+    size_t smem = (size_t)nbk * kSortWarps * 2 + 16;
     e = cudaFuncSetAttribute(sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess) {
       sort_kernel<<<b->total_channels, kSortThreads, smem, st>>>(sa);
