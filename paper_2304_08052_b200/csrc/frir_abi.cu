@@ -167,6 +167,10 @@ int frir_plan_create(int32_t fs, frir_plan** out) {
   if (e == cudaSuccess) e = upload(&dv.u, D.u.data(), D.u.size());
   if (e == cudaSuccess) e = upload(&dv.scan, scan.data(), scan.size());
   for (int i = 0; i < 6; ++i) dv.lp[i] = D.lpcoef[i];
+  for (int i = 0; i < 20; ++i) dv.ks[i] = scan[kScanKS + i];
+  for (int i = 0; i < 4; ++i) dv.mc[i] = scan[kScanStart + 4 + i];  // M^(C * 1)
+  for (int i = 0; i < 2 * kChunk; ++i) dv.fr0[i] = scan[kScanFree + i];
+  for (int i = 0; i < 4; ++i) dv.mt[i] = scan[kScanTileM + i];
   if (e != cudaSuccess) {
     set_error(std::string("plan upload: ") + cudaGetErrorString(e));
     frir_plan_destroy(p);

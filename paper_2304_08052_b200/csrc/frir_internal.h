@@ -40,13 +40,18 @@ struct DevPlan {
   double* u;           // [half2]
   double* scan;        // LP scan constants, see kernels (kScanDoubles)
   double lp[6];        // c1, c2, v0
+  // LP scan constants the render kernel reads as kernel parameters (constant
+  // bank operands, no shared-memory traffic); see lp_scan_tile
+  double ks[20];        // Kogge-Stone powers M^(C 2^s), s < 5
+  double mc[4];         // M^C (one chunk)
+  double fr0[2 * kChunk];  // row0(M^(k+1)), k < C
+  double mt[4];         // M^kTile
 };
 
 // LP scan constants: KS powers M^(C 2^s) (5 x 4), M^(C L) (32 x 4), free
 // response row0(M^(k+1)) for k < kTile (kTile x 2), M^kTile (4).
 constexpr int kScanKS = 0, kScanStart = 20, kScanFree = 20 + 128, kScanTileM = kScanFree + 2 * kTile;
 constexpr int kScanDoubles = kScanTileM + 4;
-constexpr int kScanSmem = kScanFree + 2 * kChunk;  // part the render kernel keeps in smem
 
 }  // namespace frir
 

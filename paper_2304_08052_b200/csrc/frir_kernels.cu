@@ -346,11 +346,13 @@ __device__ __forceinline__ double shfl_up_d(double v, int d) { return __shfl_up_
 
 // One variant's LP recursion over a tile: lane L owns outputs [C L, C L + C)
 // of the tile (C = kChunk).  W comes from the FP32 tile buffer; the chunk runs
-// serially in FP64 from zero state, chunks are combined with a Kogge-Stone
+// serially in FP64 from zero state, the tile's start state s enters as lane 0's
+// carry (chunk 0 ends at M^C s + e0), chunks are combined with a Kogge-Stone
 // scan of the affine maps s -> M^C s + e, and every output is corrected by the
-// free response of its chunk's true start state.  On return lp[] holds
-// LP[C L + k] and (s0, s1) = (LP[last], LP[last - 1]) of the tile.
-__device__ __forceinline__ void lp_scan_tile(const float* wbuf, const double* scan, double c1,
+// free response of its chunk's true start state.  The matrices are kernel
+// parameters (constant-bank operands).  On return lp[] holds LP[C L + k] and
+// (s0, s1) = (LP[last], LP[last - 1]) of the tile.
+__device__ __forceinline__ void lp_scan_tile(const float* wbuf, const DevPlan& P, double c1,
                                              double c2, double& s0, double& s1, int lane,
                                              double (&lp)[kChunk]) {
   const float4* w4 = reinterpret_cast<const float4*>(wbuf + kChunk * lane);
@@ -366,24 +368,23 @@ __device__ __forceinline__ void lp_scan_tile(const float* wbuf, const double* sc
     lp[k] = fma(c1, p1, fma(c2, p2, (double)wv[k]));
   }
   double e0 = lp[kChunk - 1], e1 = lp[kChunk - 2];
+  if (lane == 0) {
+    e0 = fma(P.mc[0], s0, fma(P.mc[1], s1, e0));
+    e1 = fma(P.mc[2], s0, fma(P.mc[3], s1, e1));
+  }
 #pragma unroll
   for (int s = 0; s < 5; ++s) {
     const int dd = 1 << s;
     double u0 = shfl_up_d(e0, dd), u1 = shfl_up_d(e1, dd);
     if (lane >= dd) {
-      const double* Mp = scan + kScanKS + 4 * s;
-      e0 = fma(Mp[0], u0, fma(Mp[1], u1, e0));
-      e1 = fma(Mp[2], u0, fma(Mp[3], u1, e1));
+      e0 = fma(P.ks[4 * s], u0, fma(P.ks[4 * s + 1], u1, e0));
+      e1 = fma(P.ks[4 * s + 2], u0, fma(P.ks[4 * s + 3], u1, e1));
     }
   }
   double x0 = shfl_up_d(e0, 1), x1 = shfl_up_d(e1, 1);
-  if (lane == 0) { x0 = 0.0; x1 = 0.0; }
-  const double* Ms = scan + kScanStart + 4 * lane;  // M^{C lane}
-  const double t0 = fma(Ms[0], s0, fma(Ms[1], s1, x0));
-  const double t1 = fma(Ms[2], s0, fma(Ms[3], s1, x1));
-  const double* fr = scan + kScanFree;
+  if (lane == 0) { x0 = s0; x1 = s1; }
 #pragma unroll
-  for (int k = 0; k < kChunk; ++k) lp[k] += fma(fr[2 * k], t0, fr[2 * k + 1] * t1);
+  for (int k = 0; k < kChunk; ++k) lp[k] += fma(P.fr0[2 * k], x0, P.fr0[2 * k + 1] * x1);
   s0 = shfl_d(lp[kChunk - 1], 31);
   s1 = shfl_d(lp[kChunk - 2], 31);
 }
@@ -481,15 +482,14 @@ struct Channel {
 };
 
 template <bool EARLY, int NBK>
-__global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(RenderArgs A) {
+__global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(const __grid_constant__ RenderArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const frir_plan_desc& d = A.plan.d;
   constexpr int kRow = 64 * NBK;  // doubled rows (see Channel::add)
   constexpr int V = EARLY ? 2 : 1;
   const int ncomp = d.r_h * kRow;
   float2* s_comp = reinterpret_cast<float2*>(smem);
-  double* s_scan = reinterpret_cast<double*>(smem + (size_t)ncomp * 8);
-  double* s_corr_all = s_scan + kScanSmem;                                 // [warp][V][32]
+  double* s_corr_all = reinterpret_cast<double*>(smem + (size_t)ncomp * 8);  // [warp][V][32]
   float* s_tile = reinterpret_cast<float*>(s_corr_all + kWarps * V * 32);  // [warp][V][D, W][kTile]
   int2* s_items = reinterpret_cast<int2*>(s_tile + (size_t)kWarps * V * 2 * kTile);
   float* s_head = reinterpret_cast<float*>(s_items + 32 * kWarps);          // [warp][V][D, W][64]
@@ -503,7 +503,6 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(RenderArgs A)
   for (int i = threadIdx.x; i < 128; i += blockDim.x) s_plo[i] = make_double2(A.plan.ppow_lo[2 * i], A.plan.ppow_lo[2 * i + 1]);
   for (int i = threadIdx.x; i < d.down; i += blockDim.x) s_zph[i] = make_double2(A.plan.zphase[2 * i], A.plan.zphase[2 * i + 1]);
   for (int i = threadIdx.x; i < nphi; i += blockDim.x) s_phi[i] = make_double2(A.plan.ppow_hi[2 * i], A.plan.ppow_hi[2 * i + 1]);
-  for (int i = threadIdx.x; i < kScanSmem; i += blockDim.x) s_scan[i] = A.plan.scan[i];
   __syncthreads();
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -748,19 +747,19 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(RenderArgs A)
       }
       __syncwarp();
       double lp[kChunk];
-      lp_scan_tile(wF_t, s_scan, c1, c2, sF0, sF1, lane, lp);
+      lp_scan_tile(wF_t, A.plan, c1, c2, sF0, sF1, lane, lp);
       store_chunk(outF, n_base, n2, nrow, n_c, dF_t, corrF_s, lane, lp, scale);
       if (EARLY) {
         const bool quiet = w0 > ew_hi;  // no early item feeds this tile: pure decay
         if (!quiet) {
-          lp_scan_tile(wE_t, s_scan, c1, c2, sE0, sE1, lane, lp);
+          lp_scan_tile(wE_t, A.plan, c1, c2, sE0, sE1, lane, lp);
           store_chunk(outE, n_base, n2, nrow, n_c, dE_t, corrE_s, lane, lp, scale);
         } else if (!e_dead) {
           // LP[k] = row0(M^(k+1)) . s for the whole tile; y = -LP (D = W = 0)
           const double* fr = A.plan.scan + kScanFree + 2 * kChunk * lane;  // global (L1)
 #pragma unroll
           for (int k = 0; k < kChunk; ++k) lp[k] = fma(fr[2 * k], sE0, fr[2 * k + 1] * sE1);
-          const double* Mt = A.plan.scan + kScanTileM;
+          const double* Mt = A.plan.mt;
           const double n0v = fma(Mt[0], sE0, Mt[1] * sE1), n1v = fma(Mt[2], sE0, Mt[3] * sE1);
           sE0 = n0v;
           sE1 = n1v;
@@ -853,7 +852,7 @@ static int table_blocks(const frir_plan_desc& d) { return (d.sup + 31) / 32; }
 
 static size_t render_smem(const frir_plan_desc& d, bool early) {
   const int v = early ? 2 : 1;
-  return (size_t)d.r_h * 64 * table_blocks(d) * 8 + kScanSmem * 8 + (size_t)kWarps * v * 32 * 8 +
+  return (size_t)d.r_h * 64 * table_blocks(d) * 8 + (size_t)kWarps * v * 32 * 8 +
          (size_t)kWarps * v * 2 * kTile * 4 + (size_t)kWarps * 32 * 8 +
          (size_t)kWarps * v * 2 * 64 * 4 + (size_t)(128 + d.down + d.horizon / 128 + 1) * 16 +
          (size_t)kWarps * 2 * lt_cap(d) * 8;
