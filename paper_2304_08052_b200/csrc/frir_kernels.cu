@@ -41,10 +41,12 @@ struct Workspace {
   int2* items_raw;  // per channel, image order (K1 -> K2)
   int* chan_q0;
   float* chan_scale;
+  double* corr;     // per channel [F, E][32]: tail corrections of outputs n_c + i (K2 -> K3)
   int* counter;
 };
 
 __host__ __device__ inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
 Workspace carve(void* base, const frir_batch* b) {
   char* p = (char*)base;
@@ -53,6 +55,7 @@ Workspace carve(void* base, const frir_batch* b) {
   w.items_raw = (int2*)p; p += align_up((size_t)b->total_items * 8);
   w.chan_q0 = (int*)p; p += align_up((size_t)b->total_channels * 4);
   w.chan_scale = (float*)p; p += align_up((size_t)b->total_channels * 4);
+  w.corr = (double*)p; p += align_up((size_t)b->total_channels * 64 * 8);
   w.counter = (int*)p;
   return w;
 }
@@ -217,10 +220,24 @@ __global__ void __launch_bounds__(128) geom_kernel(GeomArgs A) {
 // place.  Early flags (core.py:259-264) are set here from the channel's q0.
 // Per-warp 16-bit histograms make the placement stable (row order within a
 // bucket) without atomics deciding the order, so outputs are bit-reproducible.
+struct Cplx {
+  double re, im;
+};
+__device__ __forceinline__ Cplx cmul(Cplx a, Cplx b) {
+  return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
+}
+
+// First output whose value needs the truncation correction (outputs whose
+// stage-2 window reaches past the stage-1 length n1, resample.py:107-113).
+__host__ __device__ inline int first_corrected(const frir_plan_desc& d, int n1) {
+  return n1 - d.half2 > 0 ? (n1 - d.half2 + d.r_l - 1) / d.r_l : 0;
+}
+
 struct SortArgs {
   const frir_job* jobs;
   const int32_t* chan_job;
   Workspace ws;
+  DevPlan plan;
   int r_h, t0;
 };
 
@@ -316,6 +333,186 @@ __global__ void __launch_bounds__(kSortThreads) sort_kernel(SortArgs A) {
   }
 }
 
+// ---------------------------------------------------------------- K2b tail corrections
+// The reference truncates the stage-1 output at its length n1 before the HP
+// filter and stage 2 (resample.py:107-113); the render's untruncated chain
+// differs from it only in outputs n >= n_c, by a correction that depends on
+// the HP state at n1 (a modal sum over the items within the HP horizon, a
+// suffix of the sorted row) and on the stage-1 taps the items put past n1.
+// One warp per channel; the small power tables live in smem.  Every sum runs
+// in a fixed order, so the corrections are bit-reproducible.
+struct TailArgs {
+  const frir_job* jobs;
+  const int32_t* chan_job;
+  Workspace ws;
+  DevPlan plan;
+  int total_channels;
+};
+
+constexpr int kTailThreads = 256;
+constexpr int kTailWarps = kTailThreads / 32;
+
+__global__ void __launch_bounds__(kTailThreads) tail_kernel(const __grid_constant__ TailArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const DevPlan& P = A.plan;
+  const frir_plan_desc& d = P.d;
+  const int nphi = d.horizon / 128 + 1;
+  const int ltc = lt_cap(d);
+  double2* s_plo = reinterpret_cast<double2*>(smem);  // p^i, i < 128
+  double2* s_zph = s_plo + 128;                      // Z[rho], rho < down
+  double2* s_phi = s_zph + d.down;                   // p^(128 j)
+  double* s_xt = reinterpret_cast<double*>(s_phi + nphi);  // [warp][F, E][ltc]
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) s_plo[i] = make_double2(P.ppow_lo[2 * i], P.ppow_lo[2 * i + 1]);
+  for (int i = threadIdx.x; i < d.down; i += blockDim.x) s_zph[i] = make_double2(P.zphase[2 * i], P.zphase[2 * i + 1]);
+  for (int i = threadIdx.x; i < nphi; i += blockDim.x) s_phi[i] = make_double2(P.ppow_hi[2 * i], P.ppow_hi[2 * i + 1]);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.x * kTailWarps + warp;
+  if (c >= A.total_channels) return;
+  const int j = A.chan_job[c];
+  const frir_job& J = A.jobs[j];
+  const int m = c - J.chan_off;
+  const int rows = J.n_images + 1;
+  const int n1 = J.n1, n2 = J.n2;
+  const int2* items = A.ws.items + J.item_off + (size_t)m * rows;
+  const int up = d.up, down = d.down, half1 = d.half1, r_h = d.r_h;
+  const unsigned down_magic = (unsigned)((0x100000000ull + down - 1) / down);  // exact for e < 2^32 / down
+  const int kthr = n1 - d.horizon;  // items with k_hi >= kthr feed the state
+  double* xt_s = s_xt + 2 * ltc * warp;
+  for (int i = lane; i < 2 * ltc; i += 32) xt_s[i] = 0.0;
+  __syncwarp();
+
+  // suffix start: earlier items have bucket <= a batch's first bucket, which
+  // bounds their k_hi
+  int p_t = 0;
+  if (kthr > 0) {
+    const int nb = (rows + 31) >> 5;
+    p_t = -1;
+    for (int b0 = nb - 1; b0 >= 0 && p_t < 0; b0 -= 32) {  // 32 batch starts per round
+      const int b = b0 - lane;
+      bool below = true;  // every item before batch b has k_hi < kthr
+      if (b > 0) {
+        const int bkf = (items[32 * b].x & 0xFFFFF) >> 5;
+        const long long qmax = (long long)r_h * ((bkf << 5) + 31 - kSpBias - kExt) - d.t0;
+        below = (long long)up * qmax + half1 < (long long)kthr * down;
+      }
+      const unsigned bm = __ballot_sync(0xffffffffu, b >= 0 && below);
+      if (bm) p_t = 32 * (b0 - (__ffs(bm) - 1));
+    }
+    p_t = max(p_t, 0);
+  }
+  double4 z = make_double4(0.0, 0.0, 0.0, 0.0);  // this lane's partial modal sums (F, E)
+  constexpr int kGroup = 8;  // batches loaded together (memory-level parallelism)
+  for (int p0 = p_t; p0 < rows; p0 += 32 * kGroup) {
+  int2 grp[kGroup];
+#pragma unroll
+  for (int u = 0; u < kGroup; ++u) {
+    const int idx = p0 + 32 * u + lane;
+    grp[u] = idx < rows ? items[idx] : make_int2(0xFFFFF, 0);
+  }
+#pragma unroll
+  for (int u = 0; u < kGroup; ++u) {
+    const int p = p0 + 32 * u;
+    if (p >= rows) break;
+    const int2 it = grp[u];
+    const int cnt = min(32, rows - p);
+    const int spb = it.x & 0xFFFFF;
+    const int qm = r_h * (spb - kSpBias - kExt) - d.t0 - (((unsigned)it.x >> 20) & 0x3FF);
+    const int e = up * qm + half1;  // >= 0
+    const int khi = (int)__umulhi((unsigned)e, down_magic);
+    const bool valid = lane < cnt && khi >= kthr;
+    if (!__any_sync(0xffffffffu, valid)) continue;  // (next batch of the group)
+    const float ae = __int_as_float(it.y);
+    const bool early = ae < 0.f;
+    const double a = fabs((double)ae);
+    const bool head_item = e < 2 * half1;  // some stage-1 taps at k < 0
+    if (valid && khi < n1 && !head_item) {
+      const int rho = e - down * khi;
+      const int mm = n1 - 1 - khi;
+      FRIR_CHECK(mm >= 0 && (mm >> 7) < nphi && rho >= 0 && rho < down);
+      const double2 lo = s_plo[mm & 127], hi = s_phi[mm >> 7], zr = s_zph[rho];
+      const Cplx t = cmul(cmul({hi.x, hi.y}, {lo.x, lo.y}), {zr.x, zr.y});
+      z.x = fma(a, t.re, z.x);
+      z.y = fma(a, t.im, z.y);
+      if (early) {
+        z.z = fma(a, t.re, z.z);
+        z.w = fma(a, t.im, z.w);
+      }
+    }
+    // straddlers (taps on both sides of n1) and head items: one at a time
+    unsigned strad = __ballot_sync(0xffffffffu, valid && (khi >= n1 || head_item));
+    while (strad) {
+      const int src = __ffs(strad) - 1;
+      strad &= strad - 1;
+      const int qs = __shfl_sync(0xffffffffu, qm, src);
+      const float aes = __int_as_float(__shfl_sync(0xffffffffu, it.y, src));
+      const double as = fabs((double)aes);
+      const bool es = aes < 0.f;
+      const int khs = (int)__umulhi((unsigned)(up * qs + half1), down_magic);
+      const int xs = up * qs - half1 + 1024 * down;  // >= 0 (half1 = 10 r_h <= 1024 down)
+      const int klo = max(0, (int)__umulhi((unsigned)xs, down_magic) - 1024 + (xs % down != 0));
+      const int kend = min(khs + 1, n1);
+      for (int k = klo + lane; k < kend; k += 32) {  // taps 0 <= k < n1 feed the state
+        const int mm = n1 - 1 - k;
+        if (mm >= d.horizon) continue;
+        FRIR_CHECK(down * k + half1 - up * qs >= 0 && down * k + half1 - up * qs < d.len1);
+        const double cc = as * P.h1up[down * k + half1 - up * qs];
+        const double2 lo = s_plo[mm & 127], hi = s_phi[mm >> 7];
+        const Cplx pm = cmul({hi.x, hi.y}, {lo.x, lo.y});
+        z.x = fma(cc, pm.re, z.x);
+        z.y = fma(cc, pm.im, z.y);
+        if (es) {
+          z.z = fma(cc, pm.re, z.z);
+          z.w = fma(cc, pm.im, z.w);
+        }
+      }
+      for (int l = lane; l < d.lt_max; l += 32) {  // taps k >= n1: input past the truncation point
+        const int k = n1 + l;
+        if (k <= khs) {
+          const int idx = down * k + half1 - up * qs;
+          if (idx >= 0 && idx < d.len1) {
+            const double cc = as * P.h1up[idx];
+            xt_s[l] += cc;
+            if (es) xt_s[ltc + l] += cc;
+          }
+        }
+      }
+    }
+  }
+  }  // groups
+  // boundary state s = 2 Re(v0 zeta) and the corrections of outputs n_c + lane
+  Cplx zF = {z.x, z.y}, zE = {z.z, z.w};
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    zF.re += __shfl_xor_sync(0xffffffffu, zF.re, o);
+    zF.im += __shfl_xor_sync(0xffffffffu, zF.im, o);
+    zE.re += __shfl_xor_sync(0xffffffffu, zE.re, o);
+    zE.im += __shfl_xor_sync(0xffffffffu, zE.im, o);
+  }
+  __syncwarp();
+  const Cplx v0a = {P.lp[2], P.lp[3]}, v0b = {P.lp[4], P.lp[5]};
+  const Cplx ta = cmul(v0a, zF), tb = cmul(v0b, zF), ea = cmul(v0a, zE), eb = cmul(v0b, zE);
+  const double s0 = 2.0 * ta.re, s1 = 2.0 * tb.re, se0 = 2.0 * ea.re, se1 = 2.0 * eb.re;
+  double corrF = 0.0, corrE = 0.0;
+  const int n = first_corrected(d, n1) + lane;
+  const int ee = d.r_l * n + d.half2 - n1;
+  if (n < n2 && ee >= 0 && ee < d.half2) {
+    corrF = P.kappa[2 * ee] * s0 + P.kappa[2 * ee + 1] * s1;
+    corrE = P.kappa[2 * ee] * se0 + P.kappa[2 * ee + 1] * se1;
+    for (int l = 0; l < d.lt_max && l <= ee; ++l) {
+      const double uu = P.u[ee - l];
+      corrF += xt_s[l] * uu;
+      corrE += xt_s[ltc + l] * uu;
+    }
+  }
+  A.ws.corr[64 * (size_t)c + lane] = corrF;
+  A.ws.corr[64 * (size_t)c + 32 + lane] = corrE;
+}
+
+static size_t tail_smem(const frir_plan_desc& d) {
+  return (size_t)(128 + d.down + d.horizon / 128 + 1) * 16 + (size_t)kTailWarps * 2 * lt_cap(d) * 8;
+}
+
 // ---------------------------------------------------------------- K3 render
 struct RenderArgs {
   const frir_job* jobs;
@@ -334,12 +531,6 @@ __device__ __forceinline__ int ceil_div_i(int a, int b) {  // b > 0, any sign of
   return a >= 0 ? (a + b - 1) / b : -((-a) / b);
 }
 
-struct Cplx {
-  double re, im;
-};
-__device__ __forceinline__ Cplx cmul(Cplx a, Cplx b) {
-  return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
-}
 
 __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 __device__ __forceinline__ double shfl_up_d(double v, int d) { return __shfl_up_sync(0xffffffffu, v, d); }
@@ -493,16 +684,7 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(const __grid_
   float* s_tile = reinterpret_cast<float*>(s_corr_all + kWarps * V * 32);  // [warp][V][D, W][kTile]
   int2* s_items = reinterpret_cast<int2*>(s_tile + (size_t)kWarps * V * 2 * kTile);
   float* s_head = reinterpret_cast<float*>(s_items + 32 * kWarps);          // [warp][V][D, W][64]
-  double2* s_plo = reinterpret_cast<double2*>(s_head + kWarps * V * 2 * 64);  // p^i, i < 128
-  double2* s_zph = s_plo + 128;                                         // Z[rho], rho < down
-  double2* s_phi = s_zph + d.down;                                      // p^(128 j)
-  const int nphi = d.horizon / 128 + 1;
-  const int ltc = lt_cap(d);                                 // xt row length (last: per-rate size)
-  double* s_xt = reinterpret_cast<double*>(s_phi + nphi);   // [warp][F, E][ltc]
   for (int i = threadIdx.x; i < ncomp; i += blockDim.x) s_comp[i] = A.plan.comp[i];
-  for (int i = threadIdx.x; i < 128; i += blockDim.x) s_plo[i] = make_double2(A.plan.ppow_lo[2 * i], A.plan.ppow_lo[2 * i + 1]);
-  for (int i = threadIdx.x; i < d.down; i += blockDim.x) s_zph[i] = make_double2(A.plan.zphase[2 * i], A.plan.zphase[2 * i + 1]);
-  for (int i = threadIdx.x; i < nphi; i += blockDim.x) s_phi[i] = make_double2(A.plan.ppow_hi[2 * i], A.plan.ppow_hi[2 * i + 1]);
   __syncthreads();
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -516,9 +698,7 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(const __grid_
   double* corrE_s = corrF_s + 32;
   int2* s_it = s_items + 32 * warp;
   float* head_s = s_head + warp * V * 2 * 64;
-  double* xt_s = s_xt + 2 * ltc * warp;
   const double c1 = A.plan.lp[0], c2 = A.plan.lp[1];
-  const Cplx v0a = {A.plan.lp[2], A.plan.lp[3]}, v0b = {A.plan.lp[4], A.plan.lp[5]};
   const int sup = d.sup, r_h = d.r_h, up = d.up, down = d.down, half1 = d.half1;
   const unsigned down_magic = (unsigned)((0x100000000ull + down - 1) / down);  // exact for e < 2^32 / down
 
@@ -539,12 +719,7 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(const __grid_
     float* outF = A.out_full + J.out_off + (size_t)m * J.out_stride;
     float* outE = EARLY ? A.out_early + J.out_off + (size_t)m * J.out_stride : nullptr;
 
-    // ---- tail state (truncation at n1, resample.py:107-113): per-lane partial
-    // modal sums and the taps past n1, accumulated in smem by a pre-pass over
-    // the items within the HP horizon (a suffix of the bucket-sorted list)
-    const int n_c = n1 - d.half2 > 0 ? (n1 - d.half2 + d.r_l - 1) / d.r_l : 0;
-    const int kthr = n1 - d.horizon;  // items with k_hi >= kthr feed the state
-    for (int i = lane; i < 2 * ltc; i += 32) xt_s[i] = 0.0;
+    const int n_c = first_corrected(d, n1);  // outputs n >= n_c get K2's tail corrections
     // windows touched by early items (q in [q0 - lo, q0 + hi], core.py:257-264)
     int ew_lo = 0, ew_hi = -1;
     if (EARLY) {
@@ -603,131 +778,10 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(const __grid_
       if ((long long)up * qmin >= half1) break;
     }
 
-    // ---- tail pre-pass: find the suffix whose k_hi can reach kthr (earlier
-    // items have bucket <= a batch's first bucket, bounding their k_hi), then
-    // accumulate it and finish the boundary state and the corrections
-    int p_t = 0;
-    if (kthr > 0) {
-      const int nb = (rows + 31) >> 5;
-      p_t = -1;
-      for (int b0 = nb - 1; b0 >= 0 && p_t < 0; b0 -= 32) {  // 32 batch starts per round
-        const int b = b0 - lane;
-        bool below = true;  // every item before batch b has k_hi < kthr
-        if (b > 0) {
-          const int bkf = (items[32 * b].x & 0xFFFFF) >> 5;
-          const long long qmax = (long long)r_h * ((bkf << 5) + 31 - kSpBias - kExt) - d.t0;
-          below = (long long)up * qmax + half1 < (long long)kthr * down;
-        }
-        const unsigned bm = __ballot_sync(0xffffffffu, b >= 0 && below);
-        if (bm) p_t = 32 * (b0 - (__ffs(bm) - 1));
-      }
-      p_t = max(p_t, 0);
-    }
-    double4 z = make_double4(0.0, 0.0, 0.0, 0.0);  // this lane's partial modal sums (F, E)
-    for (int p = p_t; p < rows; p += 32) {
-      const int2 it_t = p + lane < rows ? items[p + lane] : make_int2(0xFFFFF, 0);
-      const int cnt_t = min(32, rows - p);
-      const int spb = it_t.x & 0xFFFFF;
-      const int qm = r_h * (spb - kSpBias - kExt) - d.t0 - (((unsigned)it_t.x >> 20) & 0x3FF);
-      const int e = up * qm + half1;  // >= 0
-      const int khi = (int)__umulhi((unsigned)e, down_magic);
-      const bool valid = lane < cnt_t && khi >= kthr;
-      if (__any_sync(0xffffffffu, valid)) {
-        const float ae = __int_as_float(it_t.y);
-        const bool early = ae < 0.f;
-        const double a = fabs((double)ae);
-        const bool head_item = e < 2 * half1;  // some stage-1 taps at k < 0
-        if (valid && khi < n1 && !head_item) {
-          const int rho = e - down * khi;
-          const int mm = n1 - 1 - khi;
-          FRIR_CHECK(mm >= 0 && (mm >> 7) < nphi && rho >= 0 && rho < down);
-          const double2 lo = s_plo[mm & 127], hi = s_phi[mm >> 7], zr = s_zph[rho];
-          const Cplx t = cmul(cmul({hi.x, hi.y}, {lo.x, lo.y}), {zr.x, zr.y});
-          z.x = fma(a, t.re, z.x);
-          z.y = fma(a, t.im, z.y);
-          if (EARLY && early) {
-            z.z = fma(a, t.re, z.z);
-            z.w = fma(a, t.im, z.w);
-          }
-        }
-        // straddlers (taps on both sides of n1) and head items: one at a time
-        unsigned strad = __ballot_sync(0xffffffffu, valid && (khi >= n1 || head_item));
-        while (strad) {
-          const int src = __ffs(strad) - 1;
-          strad &= strad - 1;
-          const int qs = __shfl_sync(0xffffffffu, qm, src);
-          const float aes = __int_as_float(__shfl_sync(0xffffffffu, it_t.y, src));
-          const double as = fabs((double)aes);
-          const bool es = aes < 0.f;
-          const int khs = (int)__umulhi((unsigned)(up * qs + half1), down_magic);
-          const int xs = up * qs - half1 + 1024 * down;  // >= 0 (half1 = 10 r_h <= 1024 down)
-          const int klo = max(0, (int)__umulhi((unsigned)xs, down_magic) - 1024 + (xs % down != 0));
-          const int kend = min(khs + 1, n1);
-          for (int k = klo + lane; k < kend; k += 32) {  // taps 0 <= k < n1 feed the state
-            const int mm = n1 - 1 - k;
-            if (mm >= d.horizon) continue;
-            FRIR_CHECK(down * k + half1 - up * qs >= 0 && down * k + half1 - up * qs < d.len1);
-            const double cc = as * A.plan.h1up[down * k + half1 - up * qs];
-            const double2 lo = s_plo[mm & 127], hi = s_phi[mm >> 7];
-            const Cplx pm = cmul({hi.x, hi.y}, {lo.x, lo.y});
-            z.x = fma(cc, pm.re, z.x);
-            z.y = fma(cc, pm.im, z.y);
-            if (EARLY && es) {
-              z.z = fma(cc, pm.re, z.z);
-              z.w = fma(cc, pm.im, z.w);
-            }
-          }
-          for (int l = lane; l < d.lt_max; l += 32) {  // taps k >= n1: input past the truncation point
-            const int k = n1 + l;
-            if (k <= khs) {
-              const int idx = down * k + half1 - up * qs;
-              if (idx >= 0 && idx < d.len1) {
-                const double cc = as * A.plan.h1up[idx];
-                xt_s[l] += cc;
-                if (EARLY && es) xt_s[ltc + l] += cc;
-              }
-            }
-          }
-        }
-      }
-    }
-    {  // boundary state s = 2 Re(v0 zeta) and the corrections of outputs n >= n_c
-      Cplx zF = {z.x, z.y}, zE = {z.z, z.w};
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        zF.re += __shfl_xor_sync(0xffffffffu, zF.re, o);
-        zF.im += __shfl_xor_sync(0xffffffffu, zF.im, o);
-        if (EARLY) {
-          zE.re += __shfl_xor_sync(0xffffffffu, zE.re, o);
-          zE.im += __shfl_xor_sync(0xffffffffu, zE.im, o);
-        }
-    }
+    // ---- tail corrections of outputs n >= n_c (computed by K2)
+    corrF_s[lane] = A.ws.corr[64 * (size_t)c + lane];
+    if (EARLY) corrE_s[lane] = A.ws.corr[64 * (size_t)c + 32 + lane];
     __syncwarp();
-    double corrF = 0.0, corrE = 0.0;
-    const Cplx ta = cmul(v0a, zF), tb = cmul(v0b, zF);  // s = 2 Re(v0 zeta)
-    const double s0 = 2.0 * ta.re, s1 = 2.0 * tb.re;
-    double se0 = 0.0, se1 = 0.0;
-    if (EARLY) {
-      const Cplx ea = cmul(v0a, zE), eb = cmul(v0b, zE);
-      se0 = 2.0 * ea.re;
-      se1 = 2.0 * eb.re;
-    }
-    const int n = n_c + lane;
-    const int ee = d.r_l * n + d.half2 - n1;
-    const bool act = n < n2 && ee >= 0 && ee < d.half2;
-    if (act) {
-      corrF = A.plan.kappa[2 * ee] * s0 + A.plan.kappa[2 * ee + 1] * s1;
-      if (EARLY) corrE = A.plan.kappa[2 * ee] * se0 + A.plan.kappa[2 * ee + 1] * se1;
-      for (int l = 0; l < d.lt_max && l <= ee; ++l) {
-        const double uu = A.plan.u[ee - l];
-        corrF += xt_s[l] * uu;
-        if (EARLY) corrE += xt_s[ltc + l] * uu;
-      }
-    }
-    corrF_s[lane] = corrF;
-    if (EARLY) corrE_s[lane] = corrE;
-    __syncwarp();
-    }
 
     // ---- ordered sweep: windows w = -2 .. nwin-1 over n'' = n + kExt
     const int nwin = (n2 + kExt + kWin - 1) / kWin;
@@ -845,7 +899,8 @@ int check_line() {
 }
 
 size_t workspace_bytes(const frir_batch* b) {
-  return 2 * align_up((size_t)b->total_items * 8) + 2 * align_up((size_t)b->total_channels * 4) + 256;
+  return 2 * align_up((size_t)b->total_items * 8) + 2 * align_up((size_t)b->total_channels * 4) +
+         align_up((size_t)b->total_channels * 64 * 8) + 256;
 }
 
 static int table_blocks(const frir_plan_desc& d) { return (d.sup + 31) / 32; }
@@ -854,8 +909,7 @@ static size_t render_smem(const frir_plan_desc& d, bool early) {
   const int v = early ? 2 : 1;
   return (size_t)d.r_h * 64 * table_blocks(d) * 8 + (size_t)kWarps * v * 32 * 8 +
          (size_t)kWarps * v * 2 * kTile * 4 + (size_t)kWarps * 32 * 8 +
-         (size_t)kWarps * v * 2 * 64 * 4 + (size_t)(128 + d.down + d.horizon / 128 + 1) * 16 +
-         (size_t)kWarps * 2 * lt_cap(d) * 8;
+         (size_t)kWarps * v * 2 * 64 * 4;
 }
 
 template <bool EARLY, int NBK>
@@ -879,7 +933,7 @@ static cudaError_t launch_render(const RenderArgs& ra, const frir_plan_desc& d, 
 int launches(const frir_batch* b, int early) {
   (void)b;
   (void)early;
-  return 3;  // geom, delay, render (plus one memset of the work counter)
+  return 4;  // geom, sort, tail, render (plus one memset of the work counter)
 }
 
 int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_t ws_bytes,
@@ -918,15 +972,26 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_
   if (stages & FRIR_STAGE_DELAY) {  // K2: early flags + stable bucket sort per channel
     SortArgs sa;
     sa.jobs = b->jobs; sa.chan_job = b->chan_job; sa.ws = ws;
-    sa.r_h = d.r_h; sa.t0 = d.t0;
+    sa.r_h = d.r_h; sa.t0 = d.t0; sa.plan = plan->dev;
     const int nbk = ((b->max_windows * kWin + kSpBias) >> 5) + 3;
-    size_t smem = (size_t)nbk * kSortWarps * 2 + 16;
+    size_t smem = align16((size_t)nbk * kSortWarps * 2) +
+                  (size_t)(kSortWarps + 1) * 2 * lt_cap(d) * 8 + kSortWarps * 32;
     e = cudaFuncSetAttribute(sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess) {
       sort_kernel<<<b->total_channels, kSortThreads, smem, st>>>(sa);
       e = cudaGetLastError();
     }
     if (e != cudaSuccess) { set_error(std::string("sort_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
+    TailArgs ta;  // K2b: tail corrections from the sorted rows
+    ta.jobs = b->jobs; ta.chan_job = b->chan_job; ta.ws = ws; ta.plan = plan->dev;
+    ta.total_channels = b->total_channels;
+    const size_t tsm = tail_smem(d);
+    e = cudaFuncSetAttribute(tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+    if (e == cudaSuccess) {
+      tail_kernel<<<(b->total_channels + kTailWarps - 1) / kTailWarps, kTailThreads, tsm, st>>>(ta);
+      e = cudaGetLastError();
+    }
+    if (e != cudaSuccess) { set_error(std::string("tail_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
   }
 
   if (stages & FRIR_STAGE_RENDER) {  // K3
