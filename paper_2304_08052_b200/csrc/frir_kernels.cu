@@ -66,11 +66,28 @@ Workspace carve(void* base, const frir_batch* b) {
 __device__ __forceinline__ void image_position(const frir_job& J, double dist, double az,
                                                double el, double* x, double* y, double* z) {
   // params.py:138-146 sph_to_cart; params.py:149-159 center + offset
-  double ce = cos(el), se = sin(el), ca = cos(az), sa = sin(az);
+  double ce, se, ca, sa;  // sincos == (sin, cos) bit for bit (tools/checks/sincos_identity.cu)
+  sincos(el, &se, &ce);
+  sincos(az, &sa, &ca);
   double dce = __dmul_rn(dist, ce);
   *x = __dadd_rn(J.center[0], __dmul_rn(dce, ca));
   *y = __dadd_rn(J.center[1], __dmul_rn(dce, sa));
   *z = __dadd_rn(J.center[2], __dmul_rn(dist, se));
+}
+
+// Words o .. o + 3 of the 8-word concatenation a|b (o in [0, 4)), with static
+// register indices only (a runtime-indexed array would live in local memory).
+__device__ __forceinline__ u64x4 words4(const u64x4& a, const u64x4& b, int o) {
+  u64x4 r;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint64_t c0 = a.v[k];
+    const uint64_t c1 = k + 1 < 4 ? a.v[(k + 1) & 3] : b.v[(k + 1) & 3];
+    const uint64_t c2 = k + 2 < 4 ? a.v[(k + 2) & 3] : b.v[(k + 2) & 3];
+    const uint64_t c3 = k + 3 < 4 ? a.v[(k + 3) & 3] : b.v[(k + 3) & 3];
+    r.v[k] = o == 0 ? c0 : (o == 1 ? c1 : (o == 2 ? c2 : c3));
+  }
+  return r;
 }
 
 struct GeomArgs {
@@ -115,7 +132,7 @@ __device__ __forceinline__ int2 make_item(int q, float a, int r_h, int t0, unsig
   return make_int2((int)(spb | (phi << 20)), __float_as_int(a));
 }
 
-__global__ void __launch_bounds__(128) geom_kernel(GeomArgs A) {
+__global__ void __launch_bounds__(128, 8) geom_kernel(GeomArgs A) {
   const int j = blockIdx.x;
   const frir_job& J = A.jobs[j];
   const int I = J.n_images, rows = I + 1, M = J.n_mics;
@@ -166,11 +183,10 @@ __global__ void __launch_bounds__(128) geom_kernel(GeomArgs A) {
     const double mr1 = __dsub_rn(__ddiv_rn(c_max, J.d0), 1.0);
     const double rrm1 = __dsub_rn(J.rr_max, 1.0);
     const double prange = __dsub_rn(J.perturb_hi, J.perturb_lo);
+    const u64x4 bp = words4(bp0, bp1, (int)(wp & 3)), bu = words4(bu0, bu1, (int)(wu & 3));
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      int ip = (int)((wp & 3) + k), iu = (int)((wu & 3) + k);
-      uint64_t wpk = ip < 4 ? bp0.v[ip] : bp1.v[ip - 4];
-      uint64_t wuk = iu < 4 ? bu0.v[iu] : bu1.v[iu - 4];
+      const uint64_t wpk = bp.v[k], wuk = bu.v[k];
       th[k] = __dmul_rn(kTwoPi, u64_to_unit(bt.v[k]));                // uniform(0, 2pi), core.py:154
       ph[k] = __dadd_rn(-kHalfPi, __dmul_rn(kPi, u64_to_unit(wpk)));  // uniform(-pi/2, pi/2), :155
       // core.py:94-100 quadratic_ratio_sample
