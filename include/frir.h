@@ -192,6 +192,30 @@ int frir_simulate_stages(const frir_plan* plan, const frir_batch* batch, void* w
 /* Kernel launches frir_simulate issues for `batch` (for launch accounting). */
 int32_t frir_launch_count(const frir_plan* plan, const frir_batch* batch, int32_t early);
 
+/* ---- spatialise-and-mix consumer (mixture.py:216-332) ----
+   The batched FFT convolution runs in cuFFT on the caller's side; these are
+   the kernels around it.  All pointers are device pointers.
+
+   Spectral products of _convolve_multichannel (mixture.py:216-218):
+   filt_spec[b][j][f] *= dry_spec[b][src_of[j]][f]  (complex64, f < Fc). */
+int frir_mix_spectra(void* filt_spec, const void* dry_spec, const int32_t* src_of, int32_t B,
+                     int32_t J, int32_t K, int64_t Fc, void* stream);
+/* _power (mixture.py:221-222): out[r] = mean(y[req_row[r]][req_lo[r]:req_hi[r]]^2), FP64. */
+int frir_mix_powers(const float* y, int64_t F, const int64_t* req_row, const int32_t* req_lo,
+                    const int32_t* req_hi, int32_t n_req, double* out, void* stream);
+/* SIR / SNR gains (mixture.py:285-311): powers[b] = {p_ref, (p_int_k, p_tgt_k)
+   for k = 1..S-1, p_noise}; gains[b] = {1, g_1 .. g_{S-1}, g_noise};
+   sir_db is [B][max(S-1, 1)], snr_db [B]. */
+int frir_mix_gains(const double* powers, const double* sir_db, const double* snr_db, int32_t B,
+                   int32_t S, double* gains, void* stream);
+/* Scaled references and the mixture (mixture.py:293-313) from the convolved
+   rows y[b][j][F] (j = kM+m full of speaker k, (S+k)M+m early, 2SM+m noise):
+   outputs [B][S][M][T] (sources, early), [B][M][T] (noise, mixture); samples
+   at t >= total[b] are zero. */
+int frir_mix_combine(const float* y, const double* gains, const int32_t* total, int32_t B, int32_t S,
+                     int32_t M, int64_t F, int64_t T, float* mixture, float* sources, float* early,
+                     float* noise, void* stream);
+
 const char* frir_last_error(void);
 int32_t frir_abi_version(void);
 /* Debug builds (-DFRIR_DEBUG): source line of the first failed in-kernel

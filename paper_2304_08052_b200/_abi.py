@@ -87,6 +87,12 @@ SIGNATURES = [
      [c_void_p, ctypes.POINTER(FrirBatch), c_void_p, ctypes.c_size_t, c_void_p, c_void_p,
       c_void_p, c_void_p, c_int32]),
     ("frir_launch_count", c_int32, [c_void_p, ctypes.POINTER(FrirBatch), c_int32]),
+    ("frir_mix_spectra", c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int64, c_void_p]),
+    ("frir_mix_powers", c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p]),
+    ("frir_mix_gains", c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p]),
+    ("frir_mix_combine", c_int32,
+     [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int64, c_int64, c_void_p, c_void_p,
+      c_void_p, c_void_p, c_void_p]),
     ("frir_last_error", ctypes.c_char_p, []),
     ("frir_abi_version", c_int32, []),
     ("frir_struct_size", c_int64, [c_int32]),

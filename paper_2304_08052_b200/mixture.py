@@ -1,0 +1,279 @@
+"""Spatialise-and-mix on the GPU.
+
+Mirrors the reference's consumer of the RIR path,
+``framrir.mixture.spatialize_and_mix`` (/root/reference/pkg/src/framrir/
+mixture.py:225-332) and its ``MixtureSpec`` / ``MixtureResult`` types
+(:38-80, :107-113): same arguments, defaults, random draws (in the same order
+from the caller's ``numpy`` Generator), ``ValueError`` texts and metadata.
+
+The convolutions run batched on the device: one real FFT per dry signal
+(speakers placed at their offsets, the tiled point noise), one per filter row,
+then libfrir's kernels (``include/frir.h``: frir_mix_*) for the per-filter
+spectral products, the FP64 reference-channel powers, the SIR/SNR gains and
+the scaled references plus the mixture.  The FFTs themselves are cuFFT
+(through ``torch.fft``), the library call of this row.  ``mix_device`` is the
+batched tensor API (many utterances per launch); ``spatialize_and_mix`` is the
+drop-in for one utterance with numpy in and out.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi
+
+__all__ = ["MixtureSpec", "MixtureResult", "spatialize_and_mix", "mix_device", "fft_size"]
+
+
+def _check_range(name, rng):
+    lo, hi = rng
+    if lo > hi:
+        raise ValueError(f"{name} range is empty: {rng}")
+
+
+@dataclass
+class MixtureSpec:
+    """Sampling ranges for one training utterance (mixture.py:38-80)."""
+
+    n_speakers: int = 2
+    sir_db: tuple = (-6.0, 6.0)
+    snr_db: tuple = (10.0, 20.0)
+    min_overlap_ratio: float = 0.5
+    speaker_distance: tuple = (0.3, 6.0)
+    t60_range: tuple = (0.1, 0.7)
+    room_length: tuple = (3.0, 10.0)
+    room_width: tuple = (3.0, 10.0)
+    room_height: tuple = (2.5, 4.0)
+    elevation_range: tuple = (-np.pi / 4, np.pi / 4)
+    mic_spacings: tuple = (0.04, 0.08, 0.04)
+    sample_rate: int = 16000
+    num_images: int = 2048
+    utterance_seconds: float = 4.0
+    sir_scope: str = "full"  # "full" or "overlap" (interferer power over the overlap only)
+
+    def __post_init__(self):
+        if self.n_speakers < 1:
+            raise ValueError("need at least one speaker")
+        for name in ("sir_db", "snr_db", "speaker_distance", "t60_range", "room_length",
+                     "room_width", "room_height", "elevation_range"):
+            _check_range(name, getattr(self, name))
+        if not 0.0 <= self.min_overlap_ratio <= 1.0:
+            raise ValueError("min_overlap_ratio must be in [0, 1]")
+        if self.sir_scope not in ("full", "overlap"):
+            raise ValueError("sir_scope must be 'full' or 'overlap'")
+
+
+@dataclass
+class MixtureResult:
+    mixture: np.ndarray          # (M, N)
+    sources: list                # per speaker, (M, N) reverberant reference
+    early_sources: list          # per speaker, (M, N) early-reverb reference
+    noise: np.ndarray            # (M, N)
+    metadata: dict
+
+
+def fft_size(n: int) -> int:
+    """Power-of-two FFT length holding a linear convolution of length n."""
+    return 1 << max(0, int(n - 1).bit_length())
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def mix_device(dry, dry_len, offsets, noise, noise_len, rir_full, rir_early, rir_len, sir_db, snr_db,
+               sir_scope: str = "full"):
+    """Batched spatialise-and-mix of B utterances on one device.
+
+    dry (B, S, N) float32 with valid lengths dry_len (B, S); offsets (B, S)
+    (offsets[:, 0] == 0); noise (B, Nn) with lengths noise_len (B,);
+    rir_full (B, S + 1, M, R) float32 (the noise filter last) with valid
+    lengths rir_len (B,); rir_early (B, S, M, R) or None (then the full filter,
+    as the reference copies the full image); sir_db (B, max(S - 1, 1)) and
+    snr_db (B,) in dB.  Integer/size arguments are host arrays.  Returns a dict
+    of device tensors: mixture (B, M, T), sources and early (B, S, M, T), noise
+    (B, M, T), gains (B, S + 1) [speaker gains then the noise gain], total (B,)
+    valid lengths (T = max total).  Samples past an item's total are zero.
+    """
+    torch = _torch()
+    dev = rir_full.device
+    B, S1, M, R = rir_full.shape
+    S = S1 - 1
+    if S < 1 or dry.shape[:2] != (B, S):
+        raise ValueError("need one RIR per speaker plus one for the noise")
+    dry_len = np.asarray(dry_len, dtype=np.int64).reshape(B, S)
+    offsets = np.asarray(offsets, dtype=np.int64).reshape(B, S)
+    noise_len = np.asarray(noise_len, dtype=np.int64).reshape(B)
+    rir_len = np.asarray(rir_len, dtype=np.int64).reshape(B)
+    total = (offsets + dry_len).max(axis=1) + rir_len - 1          # mixture.py:272
+    T = int(total.max()) if B else 0
+    F = fft_size(T)
+    Fc = F // 2 + 1
+    lib = _abi.lib()
+    stream = torch.cuda.current_stream(dev).cuda_stream
+
+    # dry signals at their offsets, then the point noise tiled to the dry length (:316-319)
+    x = torch.zeros((B, S + 1, F), dtype=torch.float32, device=dev)
+    for b in range(B):
+        for k in range(S):
+            o, n = int(offsets[b, k]), int(dry_len[b, k])
+            x[b, k, o:o + n] = dry[b, k, :n]
+        dl = int(total[b] - rir_len[b] + 1)
+        nl = int(noise_len[b])
+        reps = -(-dl // nl)
+        x[b, S, :dl] = noise[b, :nl].repeat(reps)[:dl]
+    # filter rows: kM+m full of speaker k, (S+k)M+m early, 2SM+m noise
+    J = (2 * S + 1) * M
+    h = torch.zeros((B, J, F), dtype=torch.float32, device=dev)
+    for b in range(B):
+        r = int(rir_len[b])
+        h[b, :S * M, :r] = rir_full[b, :S, :, :r].reshape(S * M, r)
+        src_e = rir_early[b, :, :, :r] if rir_early is not None else rir_full[b, :S, :, :r]
+        h[b, S * M:2 * S * M, :r] = src_e.reshape(S * M, r)
+        h[b, 2 * S * M:, :r] = rir_full[b, S, :, :r]
+    src_of = torch.tensor(np.concatenate([np.repeat(np.arange(S), M), np.repeat(np.arange(S), M),
+                                          np.full(M, S)]).astype(np.int32), device=dev)
+    X = torch.fft.rfft(x, n=F)
+    H = torch.fft.rfft(h, n=F)
+    del x, h
+    _abi.check(lib.frir_mix_spectra(H.data_ptr(), X.data_ptr(), src_of.data_ptr(), B, J, S + 1, Fc,
+                                    stream), "frir_mix_spectra")
+    y = torch.fft.irfft(H, n=F)
+    del H, X
+
+    # reference-channel power requests (mixture.py:284-303, 311)
+    rows, lo, hi = [], [], []
+    for b in range(B):
+        base = b * J
+        tot = int(total[b])
+        rows.append(base); lo.append(0); hi.append(tot)                       # p_ref
+        for k in range(1, S):
+            if sir_scope == "overlap":
+                a = int(offsets[b, k])
+                e = min(tot, int(offsets[b, k] + dry_len[b, k] + rir_len[b] - 1))
+            else:
+                a, e = 0, tot
+            rows.append(base + k * M); lo.append(a); hi.append(e)           # p_int
+            rows.append(base); lo.append(a); hi.append(e)                   # p_tgt
+        rows.append(base + 2 * S * M); lo.append(0); hi.append(tot)       # p_noise
+    req_row = torch.tensor(rows, dtype=torch.int64, device=dev)
+    req_lo = torch.tensor(lo, dtype=torch.int32, device=dev)
+    req_hi = torch.tensor(hi, dtype=torch.int32, device=dev)
+    pw = torch.empty(len(rows), dtype=torch.float64, device=dev)
+    _abi.check(lib.frir_mix_powers(y.data_ptr(), F, req_row.data_ptr(), req_lo.data_ptr(),
+                                   req_hi.data_ptr(), len(rows), pw.data_ptr(), stream), "frir_mix_powers")
+    sir = torch.as_tensor(np.asarray(sir_db, dtype=np.float64).reshape(B, max(S - 1, 1)), device=dev)
+    snr = torch.as_tensor(np.asarray(snr_db, dtype=np.float64).reshape(B), device=dev)
+    gains = torch.empty((B, S + 1), dtype=torch.float64, device=dev)
+    _abi.check(lib.frir_mix_gains(pw.data_ptr(), sir.data_ptr(), snr.data_ptr(), B, S, gains.data_ptr(),
+                                  stream), "frir_mix_gains")
+    tot_d = torch.as_tensor(total.astype(np.int32), device=dev)
+    out = {
+        "mixture": torch.empty((B, M, T), dtype=torch.float32, device=dev),
+        "sources": torch.empty((B, S, M, T), dtype=torch.float32, device=dev),
+        "early": torch.empty((B, S, M, T), dtype=torch.float32, device=dev),
+        "noise": torch.empty((B, M, T), dtype=torch.float32, device=dev),
+    }
+    _abi.check(lib.frir_mix_combine(y.data_ptr(), gains.data_ptr(), tot_d.data_ptr(), B, S, M, F, T,
+                                    out["mixture"].data_ptr(), out["sources"].data_ptr(),
+                                    out["early"].data_ptr(), out["noise"].data_ptr(), stream),
+               "frir_mix_combine")
+    out["gains"] = gains
+    out["total"] = total
+    out["powers"] = pw
+    return out
+
+
+def _draw_offsets(sources, spec: MixtureSpec, rng):
+    """mixture.py:245-257: overlap-constrained offsets from the caller's rng."""
+    n0 = len(sources[0])
+    offsets = [0]
+    for k in range(1, len(sources)):
+        need = math.ceil(spec.min_overlap_ratio * min(n0, len(sources[k])))
+        hi = n0 - need
+        if hi < 0:
+            raise ValueError(f"speaker {k} is shorter than the required overlap window")
+        offsets.append(int(rng.integers(0, hi + 1)))
+    return offsets
+
+
+def _overlap_ratio(n0, off, nk):
+    return max(0, min(n0, off + nk) - off) / min(n0, nk)
+
+
+def spatialize_and_mix(sources: list, noise: np.ndarray, rirs: list, spec: MixtureSpec, rng,
+                       sir_db: list | None = None, snr_db: float | None = None,
+                       offsets: list | None = None, *, device=None) -> MixtureResult:
+    """Convolve, overlap and scale one utterance (drop-in for mixture.py:225-332).
+
+    ``rirs`` holds one RirResult per speaker plus one for the noise (last).
+    Offsets, SIR and SNR are drawn from ``rng`` exactly as the reference does
+    when not given; the arrays are computed on the GPU (FP32 samples, FP64
+    powers and gains) and returned as float64 numpy arrays like the reference.
+    """
+    torch = _torch()
+    if len(rirs) != len(sources) + 1:
+        raise ValueError("need one RIR per speaker plus one for the noise")
+    n0 = len(sources[0])
+    if offsets is None:
+        offsets = _draw_offsets(sources, spec, rng)
+    for k in range(1, len(sources)):
+        achieved = _overlap_ratio(n0, offsets[k], len(sources[k]))
+        if achieved < spec.min_overlap_ratio:
+            raise ValueError(
+                f"speaker {k} overlap ratio {achieved:.2f} is below the "
+                f"required {spec.min_overlap_ratio}"
+            )
+    S = len(sources)
+    if sir_db is None:
+        sir_db = [float(rng.uniform(*spec.sir_db)) for _ in range(S - 1)]
+    if snr_db is None:
+        snr_db = float(rng.uniform(*spec.snr_db))
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+
+    R = rirs[0].full.n_samples
+    M = rirs[0].full.samples.shape[0]
+    lens = [len(s) for s in sources]
+    N = max(lens)
+    dry = np.zeros((1, S, N), dtype=np.float32)
+    for k, s in enumerate(sources):
+        dry[0, k, :len(s)] = s
+    rf = np.zeros((1, S + 1, M, R), dtype=np.float32)
+    re = np.zeros((1, S, M, R), dtype=np.float32)
+    for k, r in enumerate(rirs):
+        rf[0, k] = r.full.samples[:, :R]
+        if k < S:
+            re[0, k] = (r.early if r.early is not None else r.full).samples[:, :R]
+    nz = np.asarray(noise, dtype=np.float32)[None, :]
+    out = mix_device(
+        torch.from_numpy(dry).to(dev), [lens], [offsets], torch.from_numpy(nz).to(dev), [len(noise)],
+        torch.from_numpy(rf).to(dev), torch.from_numpy(re).to(dev), [R],
+        [list(sir_db) if S > 1 else [0.0]], [snr_db],
+        sir_scope=spec.sir_scope,
+    )
+    T = int(out["total"][0])
+    mixture = out["mixture"][0, :, :T].double().cpu().numpy()
+    srcs = out["sources"][0, :, :, :T].double().cpu().numpy()
+    early = out["early"][0, :, :, :T].double().cpu().numpy()
+    noise_img = out["noise"][0, :, :T].double().cpu().numpy()
+    gains = out["gains"][0].cpu().numpy()
+    overlap_ratios = [_overlap_ratio(n0, offsets[k], len(sources[k])) for k in range(1, S)]
+    return MixtureResult(
+        mixture=mixture,
+        sources=[srcs[k] for k in range(S)],
+        early_sources=[early[k] for k in range(S)],
+        noise=noise_img,
+        metadata={
+            "offsets": list(offsets),
+            "gains": [float(g) for g in gains[:S]],
+            "noise_gain": float(gains[S]),
+            "sir_db": list(sir_db),
+            "snr_db": snr_db,
+            "overlap_ratios": overlap_ratios,
+        },
+    )

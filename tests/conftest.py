@@ -28,6 +28,8 @@ def golden():
         "cfg1": dict(np.load(g / "cfg1.npz")),
         "cases": dict(np.load(g / "cases.npz")),
         "cases_meta": json.loads((g / "cases.json").read_text()),
+        "mix": dict(np.load(g / "mix.npz")),
+        "mix_meta": json.loads((g / "mix.json").read_text()),
     }
 
 

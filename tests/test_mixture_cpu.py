@@ -1,0 +1,56 @@
+"""Host logic of the spatialise-and-mix drop-in (no GPU): spec validation and
+the rng draws of offsets / SIR / SNR, against the reference's texts and the
+golden cases' drawn values (mixture.py:38-80, :245-263)."""
+
+import numpy as np
+import pytest
+
+from paper_2304_08052_b200 import mixture as MX
+
+
+def test_spec_defaults_mirror_reference():
+    s = MX.MixtureSpec()
+    assert (s.n_speakers, s.sir_db, s.snr_db, s.min_overlap_ratio) == (2, (-6.0, 6.0), (10.0, 20.0), 0.5)
+    assert (s.sample_rate, s.num_images, s.utterance_seconds, s.sir_scope) == (16000, 2048, 4.0, "full")
+
+
+@pytest.mark.parametrize("kw,msg", [
+    ({"n_speakers": 0}, "need at least one speaker"),
+    ({"sir_db": (3.0, 1.0)}, "sir_db range is empty"),
+    ({"t60_range": (0.7, 0.1)}, "t60_range range is empty"),
+    ({"min_overlap_ratio": 1.5}, "min_overlap_ratio must be in"),
+    ({"sir_scope": "partial"}, "sir_scope must be"),
+])
+def test_spec_validation(kw, msg):
+    with pytest.raises(ValueError, match=msg):
+        MX.MixtureSpec(**kw)
+
+
+def test_fft_size():
+    assert MX.fft_size(1) == 1 and MX.fft_size(2) == 2 and MX.fft_size(3) == 4
+    assert MX.fft_size(70399) == 131072 and MX.fft_size(65536) == 65536
+
+
+@pytest.mark.parametrize("ci", [4, 5])
+def test_drawn_offsets_sir_snr_match_reference(golden, ci):
+    """Same rng consumption order as the reference: offsets, then SIR, then SNR."""
+    m = golden["mix_meta"][ci]
+    rng = np.random.default_rng(m["draw_seed"])
+    spec = MX.MixtureSpec(n_speakers=len(m["lens"]), sir_scope=m["scope"],
+                          min_overlap_ratio=m["min_overlap_ratio"])
+    srcs = [np.zeros(n) for n in m["lens"]]
+    offs = MX._draw_offsets(srcs, spec, rng)
+    sir = [float(rng.uniform(*spec.sir_db)) for _ in range(len(srcs) - 1)]
+    snr = float(rng.uniform(*spec.snr_db))
+    assert offs == m["offsets"] and sir == m["sir_db"] and snr == m["snr_db"]
+
+
+def test_short_source_rejected_before_compute():
+    rng = np.random.default_rng(8)
+    spec = MX.MixtureSpec(min_overlap_ratio=0.9, utterance_seconds=1.0)
+    srcs = [np.zeros(8000), np.zeros(500)]
+    with pytest.raises(ValueError, match="overlap"):
+        MX.spatialize_and_mix(srcs, np.zeros(8000), [None] * 3, spec, rng, sir_db=[0.0], snr_db=15.0,
+                              offsets=[0, 7800])
+    with pytest.raises(ValueError, match="one RIR"):
+        MX.spatialize_and_mix([np.zeros(100)], np.zeros(100), [None] * 3, spec, rng)

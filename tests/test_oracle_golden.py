@@ -92,3 +92,21 @@ def test_early_window_offsets():
 def test_index_arithmetic():
     # test_core.py:210-212
     assert math.ceil(3.43 / 343.0 * 62 * 16000) == 9920
+
+
+@pytest.mark.parametrize("ci", range(6))
+def test_mixture_port_matches_reference(golden, ci):
+    """oracle/mixture_port.py vs framrir.mixture.spatialize_and_mix outputs."""
+    from _mixcases import case
+    from oracle import mixture_port as MP
+
+    m, srcs, noise, rf, re, ref = case(golden, ci)
+    mix, pf, pe, nimg, gains, gn = MP.mix(srcs, noise, rf, re, m["offsets"], m["sir_db"], m["snr_db"],
+                                          m["scope"])
+    pk = m["peak"]
+    assert np.abs(mix - ref["mixture"]).max() / pk < 1e-6
+    for k in range(len(srcs)):
+        assert np.abs(pf[k] - ref["sources"][k]).max() / pk < 1e-6
+        assert np.abs(pe[k] - ref["early"][k]).max() / pk < 1e-6
+    assert np.abs(nimg - ref["noise"]).max() / pk < 1e-6
+    assert np.allclose(gains, m["gains"], rtol=1e-12) and math.isclose(gn, m["noise_gain"], rel_tol=1e-12)

@@ -12,6 +12,10 @@ reference.  Cases:
                       its direct indices and the reference ImageSet draws.
 * cases.npz           small scenes over 8/16/22.05/44.1/48 kHz with their
                       draws and reference outputs (float32) and FP64 peaks.
+* mix.npz / mix.json  framrir.mixture.spatialize_and_mix on small seeded
+                      inputs (explicit and rng-drawn offsets/SIR/SNR, both
+                      SIR scopes, 1-3 speakers, missing early filters, tiled
+                      noise): inputs and reference outputs (float32).
 """
 
 from __future__ import annotations
@@ -168,11 +172,77 @@ def cases():
     (OUT / "cases.json").write_text(json.dumps(meta, indent=1))
 
 
+def _decaying_filters(rng, m, r, fs=16000):
+    t = np.arange(r) / fs
+    h = rng.standard_normal((m, r)) * np.exp(-t / 0.004)[None, :]
+    h[:, 0] += 1.0
+    return h.astype(np.float32).astype(np.float64)  # stored as float32, exactly
+
+
+def mix_cases():
+    from framrir.mixture import MixtureSpec, spatialize_and_mix
+    from framrir.resample import RirFilter
+
+    specs = [
+        # (seed, M, R, lengths, noise_len, offsets, sir, snr, scope, early?, overlap_ratio)
+        (1, 2, 120, [900, 700], 900, [0, 250], [3.0], 15.0, "full", True, 0.5),
+        (2, 2, 120, [900, 700], 900, [0, 250], [-4.0], 12.0, "overlap", True, 0.5),
+        (3, 3, 100, [800], 300, [0], [], 10.0, "full", False, 0.5),
+        (4, 3, 110, [700, 600, 500], 700, [0, 150, 300], [2.0, -1.0], 18.0, "full", True, 0.3),
+        (5, 2, 100, [800, 800], 800, None, None, None, "full", True, 0.5),
+        (6, 2, 100, [800, 600], 400, None, None, None, "overlap", True, 0.6),
+    ]
+    blobs, meta = {}, []
+    for i, (seed, m, r, lens, nl, offs, sir, snr, scope, has_early, ovr) in enumerate(specs):
+        rng = np.random.default_rng(seed)
+        f32 = lambda a: a.astype(np.float32).astype(np.float64)  # noqa: E731 (stored as float32)
+        srcs = [f32(rng.standard_normal(n)) for n in lens]
+        noise = f32(rng.standard_normal(nl))
+        rirs = []
+        for k in range(len(lens) + 1):
+            hf = _decaying_filters(rng, m, r)
+            he = hf * (np.arange(r) < r // 4)[None, :]
+            full = RirFilter(samples=hf, direct_path_sample=np.zeros(m, dtype=int), sample_rate=16000)
+            early = RirFilter(samples=he, direct_path_sample=np.zeros(m, dtype=int), sample_rate=16000,
+                              kind="early") if (has_early and k < len(lens)) else None
+            rirs.append(F.RirResult(full=full, early=early))
+        spec = MixtureSpec(n_speakers=len(lens), sir_scope=scope, min_overlap_ratio=ovr)
+        draw_rng = np.random.default_rng(100 + seed)
+        res = spatialize_and_mix(srcs, noise, rirs, spec, draw_rng, sir_db=sir, snr_db=snr, offsets=offs)
+        pre = f"c{i}_"
+        for k, s_ in enumerate(srcs):
+            blobs[pre + f"src{k}"] = s_.astype(np.float32)
+        blobs[pre + "noise"] = noise.astype(np.float32)
+        for k, rr in enumerate(rirs):
+            blobs[pre + f"rirf{k}"] = rr.full.samples.astype(np.float32)
+            if rr.early is not None:
+                blobs[pre + f"rire{k}"] = rr.early.samples.astype(np.float32)
+        blobs[pre + "mixture"] = res.mixture.astype(np.float32)
+        for k in range(len(lens)):
+            blobs[pre + f"out_src{k}"] = res.sources[k].astype(np.float32)
+            blobs[pre + f"out_early{k}"] = res.early_sources[k].astype(np.float32)
+        blobs[pre + "out_noise"] = res.noise.astype(np.float32)
+        md = res.metadata
+        meta.append({"seed": seed, "M": m, "R": r, "lens": lens, "noise_len": nl, "scope": scope,
+                     "has_early": has_early, "min_overlap_ratio": ovr, "draw_seed": 100 + seed,
+                     "given": {"offsets": offs, "sir_db": sir, "snr_db": snr},
+                     "offsets": [int(o) for o in md["offsets"]], "gains": md["gains"],
+                     "noise_gain": md["noise_gain"], "sir_db": md["sir_db"], "snr_db": md["snr_db"],
+                     "overlap_ratios": md["overlap_ratios"],
+                     "peak": float(np.abs(res.mixture).max())})
+    np.savez_compressed(OUT / "mix.npz", **blobs)
+    (OUT / "mix.json").write_text(json.dumps(meta, indent=1))
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
+    if "--mix-only" in sys.argv:
+        mix_cases()
+        return
     (OUT / "kat.json").write_text(json.dumps(kat(), indent=1))
     cfg1()
     cases()
+    mix_cases()
     for f in sorted(OUT.iterdir()):
         print(f.name, f.stat().st_size)
 
