@@ -200,9 +200,25 @@ int32_t frir_launch_count(const frir_plan* plan, const frir_batch* batch, int32_
    filt_spec[b][j][f] *= dry_spec[b][src_of[j]][f]  (complex64, f < Fc). */
 int frir_mix_spectra(void* filt_spec, const void* dry_spec, const int32_t* src_of, int32_t B,
                      int32_t J, int32_t K, int64_t Fc, void* stream);
-/* _power (mixture.py:221-222): out[r] = mean(y[req_row[r]][req_lo[r]:req_hi[r]]^2), FP64. */
+/* FFT frames of the dry signals (mixture.py:274-287, 307-312): x[b][k][F] for
+   k < S holds speaker k at offsets[b][k] (lengths[b][k] samples of dry), k = S
+   the noise tiled to dry_len[b] samples; zeros elsewhere. */
+int frir_mix_pack_dry(const float* dry, int64_t dry_stride_b, int64_t dry_stride_k, const float* noise,
+                      int64_t noise_stride, const int32_t* offsets, const int32_t* lengths,
+                      const int32_t* noise_len, const int32_t* dry_len, int32_t B, int32_t S, int64_t F,
+                      float* x, void* stream);
+/* FFT frames of the filters: h[b][j][F], rows j = kM+m (full, speaker k),
+   (S+k)M+m (early; full when rir_early is NULL), 2SM+m (noise); item b's
+   filters are [S+1][M][R] at rir_full + b*full_stride_b and [>= S][M][R] at
+   rir_early + b*early_stride_b (floats); rir_len[b] valid taps. */
+int frir_mix_pack_filters(const float* rir_full, int64_t full_stride_b, const float* rir_early,
+                          int64_t early_stride_b, const int32_t* rir_len, int32_t B, int32_t S, int32_t M,
+                          int64_t R, int64_t F, float* h, void* stream);
+/* _power (mixture.py:221-222): out[r] = mean(y[req_row[r]][req_lo[r]:req_hi[r]]^2),
+   FP64, fixed-order sums; scratch holds FRIR_MIX_POWER_CHUNKS doubles per request. */
+#define FRIR_MIX_POWER_CHUNKS 32
 int frir_mix_powers(const float* y, int64_t F, const int64_t* req_row, const int32_t* req_lo,
-                    const int32_t* req_hi, int32_t n_req, double* out, void* stream);
+                    const int32_t* req_hi, int32_t n_req, double* scratch, double* out, void* stream);
 /* SIR / SNR gains (mixture.py:285-311): powers[b] = {p_ref, (p_int_k, p_tgt_k)
    for k = 1..S-1, p_noise}; gains[b] = {1, g_1 .. g_{S-1}, g_noise};
    sir_db is [B][max(S-1, 1)], snr_db [B]. */

@@ -70,6 +70,8 @@ class FrirBatch(ctypes.Structure):
 JOB_DTYPE = np.dtype(FrirJob)
 
 # (name, restype, argtypes) of every symbol include/frir.h declares.
+MIX_POWER_CHUNKS = 32  # FRIR_MIX_POWER_CHUNKS
+
 SIGNATURES = [
     ("frir_plan_create", c_int32, [c_int32, ctypes.POINTER(c_void_p)]),
     ("frir_plan_describe", c_int32, [c_void_p, ctypes.POINTER(FrirPlanDesc)]),
@@ -87,8 +89,15 @@ SIGNATURES = [
      [c_void_p, ctypes.POINTER(FrirBatch), c_void_p, ctypes.c_size_t, c_void_p, c_void_p,
       c_void_p, c_void_p, c_int32]),
     ("frir_launch_count", c_int32, [c_void_p, ctypes.POINTER(FrirBatch), c_int32]),
+    ("frir_mix_pack_dry", c_int32,
+     [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int32,
+      c_int32, c_int64, c_void_p, c_void_p]),
+    ("frir_mix_pack_filters", c_int32,
+     [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int32, c_int32, c_int32, c_int64, c_int64, c_void_p,
+      c_void_p]),
     ("frir_mix_spectra", c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int64, c_void_p]),
-    ("frir_mix_powers", c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p]),
+    ("frir_mix_powers", c_int32,
+     [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
     ("frir_mix_gains", c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p]),
     ("frir_mix_combine", c_int32,
      [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int64, c_int64, c_void_p, c_void_p,

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <string>
 
 #include "../../include/frir.h"
@@ -17,30 +18,32 @@ namespace frir {
 namespace {
 
 // spec[b][j][f] *= dry[b][src_of[j]][f], complex64 interleaved, f < Fc.
+// Grid (f blocks, J, B): one filter row per (y, z).
 __global__ void mix_spectra_kernel(float2* __restrict__ spec, const float2* __restrict__ dry,
                                    const int32_t* __restrict__ src_of, int J, int K, long Fc) {
-  const long per_item = (long)J * Fc;
-  const int b = blockIdx.y;
-  float2* s = spec + (size_t)b * per_item;
-  const float2* x = dry + (size_t)b * K * Fc;
-  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < per_item; i += (long)gridDim.x * blockDim.x) {
-    const int j = (int)(i / Fc);
-    const long f = i - (long)j * Fc;
-    const float2 h = s[i], d = x[(size_t)src_of[j] * Fc + f];
-    s[i] = make_float2(h.x * d.x - h.y * d.y, h.x * d.y + h.y * d.x);
+  const int j = blockIdx.y, b = blockIdx.z;
+  float2* s = spec + ((size_t)b * J + j) * Fc;
+  const float2* x = dry + ((size_t)b * K + src_of[j]) * Fc;
+  for (long f = blockIdx.x * (long)blockDim.x + threadIdx.x; f < Fc; f += (long)gridDim.x * blockDim.x) {
+    const float2 h = s[f], d = __ldg(x + f);
+    s[f] = make_float2(h.x * d.x - h.y * d.y, h.x * d.y + h.y * d.x);
   }
 }
 
-// Mean of squares over [lo, hi) of one row per request, FP64, fixed order.
-// req[r] = {row index into y (absolute), lo, hi}; y rows have length F.
+// Sums of squares over [lo, hi) of one row per request, split into kPowChunks
+// chunks (grid (chunks, requests)); FP64, fixed order: each chunk's block
+// reduction, then mix_gains_kernel adds the chunks in order.
+constexpr int kPowChunks = FRIR_MIX_POWER_CHUNKS;
 __global__ void mix_power_kernel(const float* __restrict__ y, const int64_t* __restrict__ req_row,
                                  const int32_t* __restrict__ req_lo, const int32_t* __restrict__ req_hi,
-                                 long F, double* __restrict__ out) {
-  const int r = blockIdx.x;
+                                 long F, double* __restrict__ part) {
+  const int r = blockIdx.y, c = blockIdx.x;
   const float* row = y + (size_t)req_row[r] * F;
   const int lo = req_lo[r], hi = req_hi[r];
+  const int span = (hi - lo + kPowChunks - 1) / kPowChunks;
+  const int a = lo + c * span, e = min(hi, a + span);
   double acc = 0.0;
-  for (int t = lo + threadIdx.x; t < hi; t += blockDim.x) {
+  for (int t = a + threadIdx.x; t < e; t += blockDim.x) {
     const double v = (double)row[t];
     acc = fma(v, v, acc);
   }
@@ -51,7 +54,18 @@ __global__ void mix_power_kernel(const float* __restrict__ y, const int64_t* __r
     if ((int)threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) out[r] = hi > lo ? s[0] / (double)(hi - lo) : 0.0 / 0.0;
+  if (threadIdx.x == 0) part[(size_t)r * kPowChunks + c] = s[0];
+}
+
+// Means from the chunk sums (fixed order).
+__global__ void mix_power_finish_kernel(const double* __restrict__ part, const int32_t* __restrict__ req_lo,
+                                        const int32_t* __restrict__ req_hi, int n_req, double* __restrict__ out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_req) return;
+  double t = 0.0;
+  for (int c = 0; c < kPowChunks; ++c) t += part[(size_t)r * kPowChunks + c];
+  const int n = req_hi[r] - req_lo[r];
+  out[r] = n > 0 ? t / (double)n : 0.0 / 0.0;
 }
 
 // Gains of mixture.py:285-311 per item from the power table
@@ -74,20 +88,18 @@ __global__ void mix_gains_kernel(const double* __restrict__ pw, const double* __
 // Scaled outputs and the mixture (mixture.py:293-313):
 //   sources[b][k][m][t] = g_k y[b][kM + m][t], early[b][k][m][t] = g_k y[b][(S + k)M + m][t],
 //   noise[b][m][t] = g_n y[b][2SM + m][t], mixture = sum_k sources + noise,
-// for t < total_b (zeros up to T).
+// for t < total_b (zeros up to T).  Grid (t blocks, M, B).
 __global__ void mix_combine_kernel(const float* __restrict__ y, const double* __restrict__ gains,
                                    const int32_t* __restrict__ total, int S, int M, long F, long T,
                                    float* __restrict__ mixture, float* __restrict__ sources,
                                    float* __restrict__ early, float* __restrict__ noise) {
-  const int b = blockIdx.y;
-  const long per_item = (long)M * T;
+  const int m = blockIdx.y, b = blockIdx.z;
   const int J = (2 * S + 1) * M;
   const float* yb = y + (size_t)b * J * F;
   const double* g = gains + (size_t)b * (S + 1);
   const int tot = total[b];
-  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < per_item; i += (long)gridDim.x * blockDim.x) {
-    const int m = (int)(i / T);
-    const long t = i - (long)m * T;
+  const float gn = (float)g[S];
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < T; t += (long)gridDim.x * blockDim.x) {
     const bool in = t < tot;
     float mix = 0.f;
     for (int k = 0; k < S; ++k) {
@@ -98,18 +110,59 @@ __global__ void mix_combine_kernel(const float* __restrict__ y, const double* __
       early[(((size_t)b * S + k) * M + m) * T + t] = ve;
       mix += vf;
     }
-    const float vn = in ? (float)g[S] * yb[(size_t)(2 * S * M + m) * F + t] : 0.f;
+    const float vn = in ? gn * yb[(size_t)(2 * S * M + m) * F + t] : 0.f;
     noise[((size_t)b * M + m) * T + t] = vn;
     mixture[((size_t)b * M + m) * T + t] = mix + vn;
   }
 }
 
-int grid_for(long n, int threads) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long want = (n + threads - 1) / threads;
-  return (int)(want < 8L * sms ? (want > 0 ? want : 1) : 8L * sms);
+// Dry signals of one FFT frame per (item, source): speakers at their offsets,
+// the point noise tiled to the dry length (mixture.py:307-312).
+// x[b][k][t], k < S: dry[b][k][t - off[b][k]] inside [0, len), else 0;
+// x[b][S][t] = noise[b][t mod nlen[b]] for t < dlen[b], else 0.
+__global__ void mix_pack_dry_kernel(const float* __restrict__ dry, long dry_stride_b, long dry_stride_k,
+                                    const float* __restrict__ noise, long noise_stride,
+                                    const int32_t* __restrict__ off, const int32_t* __restrict__ len,
+                                    const int32_t* __restrict__ nlen, const int32_t* __restrict__ dlen,
+                                    int S, long F, float* __restrict__ x) {
+  const int b = blockIdx.z, k = blockIdx.y;
+  float* row = x + ((size_t)b * (S + 1) + k) * F;
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < F; t += (long)gridDim.x * blockDim.x) {
+    float v = 0.f;
+    if (k < S) {
+      const long u = t - off[b * S + k];
+      if (u >= 0 && u < len[b * S + k]) v = dry[(size_t)b * dry_stride_b + (size_t)k * dry_stride_k + u];
+    } else if (t < dlen[b]) {
+      v = noise[(size_t)b * noise_stride + t % nlen[b]];
+    }
+    row[t] = v;
+  }
+}
+
+// Filter rows of one FFT frame each: h[b][j][t] for t < rlen[b] (zero after):
+// j = kM+m full of speaker k, (S+k)M+m early (full when early == nullptr),
+// 2SM+m the noise filter.  Per item b, rir_full + b * full_sb is [S+1][M][R]
+// and rir_early + b * early_sb is [>= S][M][R].
+__global__ void mix_pack_filters_kernel(const float* __restrict__ rir_full, long full_sb,
+                                        const float* __restrict__ rir_early, long early_sb,
+                                        const int32_t* __restrict__ rlen, int S, int M, long R, long F,
+                                        float* __restrict__ h) {
+  const int b = blockIdx.z, j = blockIdx.y;
+  const int J = (2 * S + 1) * M;
+  float* row = h + ((size_t)b * J + j) * F;
+  const float* src;
+  if (j < S * M) {
+    src = rir_full + (size_t)b * full_sb + ((size_t)(j / M) * M + j % M) * R;
+  } else if (j < 2 * S * M) {
+    const int jj = j - S * M;
+    src = rir_early ? rir_early + (size_t)b * early_sb + ((size_t)(jj / M) * M + jj % M) * R
+                    : rir_full + (size_t)b * full_sb + ((size_t)(jj / M) * M + jj % M) * R;
+  } else {
+    src = rir_full + (size_t)b * full_sb + ((size_t)S * M + (j - 2 * S * M)) * R;
+  }
+  const int r = rlen[b];
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < F; t += (long)gridDim.x * blockDim.x)
+    row[t] = t < r ? src[t] : 0.f;
 }
 
 int launched(const char* what) {
@@ -128,6 +181,37 @@ using namespace frir;
 
 extern "C" {
 
+int frir_mix_pack_dry(const float* dry, int64_t dry_stride_b, int64_t dry_stride_k, const float* noise,
+                      int64_t noise_stride, const int32_t* offsets, const int32_t* lengths,
+                      const int32_t* noise_len, const int32_t* dry_len, int32_t B, int32_t S, int64_t F,
+                      float* x, void* stream) {
+  if (!dry || !noise || !offsets || !lengths || !noise_len || !dry_len || !x || B < 0 || S < 1 || F < 1) {
+    set_error("frir_mix_pack_dry: invalid argument");
+    return FRIR_EINVAL;
+  }
+  if (B == 0) return FRIR_OK;
+  dim3 grid((unsigned)((F + 1023) / 1024 < 64 ? (F + 1023) / 1024 : 64), S + 1, B);
+  mix_pack_dry_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(dry, (long)dry_stride_b, (long)dry_stride_k, noise,
+                                                             (long)noise_stride, offsets, lengths, noise_len,
+                                                             dry_len, S, (long)F, x);
+  return launched("mix_pack_dry_kernel");
+}
+
+int frir_mix_pack_filters(const float* rir_full, int64_t full_stride_b, const float* rir_early,
+                          int64_t early_stride_b, const int32_t* rir_len, int32_t B, int32_t S, int32_t M,
+                          int64_t R, int64_t F, float* h, void* stream) {
+  if (!rir_full || !rir_len || !h || B < 0 || S < 1 || M < 1 || R < 1 || F < R) {
+    set_error("frir_mix_pack_filters: invalid argument");
+    return FRIR_EINVAL;
+  }
+  if (B == 0) return FRIR_OK;
+  dim3 grid((unsigned)((F + 1023) / 1024 < 64 ? (F + 1023) / 1024 : 64), (2 * S + 1) * M, B);
+  mix_pack_filters_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(rir_full, (long)full_stride_b, rir_early,
+                                                                 (long)early_stride_b, rir_len, S, M, (long)R,
+                                                                 (long)F, h);
+  return launched("mix_pack_filters_kernel");
+}
+
 int frir_mix_spectra(void* filt_spec, const void* dry_spec, const int32_t* src_of, int32_t B,
                      int32_t J, int32_t K, int64_t Fc, void* stream) {
   if (!filt_spec || !dry_spec || !src_of || B < 0 || J < 0 || K < 1 || Fc < 1) {
@@ -135,20 +219,23 @@ int frir_mix_spectra(void* filt_spec, const void* dry_spec, const int32_t* src_o
     return FRIR_EINVAL;
   }
   if (B == 0 || J == 0) return FRIR_OK;
-  dim3 grid(grid_for((long)J * Fc, 256) / (B > 8 ? 8 : 1) + 1, B);
+  dim3 grid((unsigned)std::min<long>((Fc + 1023) / 1024, 64), J, B);
   mix_spectra_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((float2*)filt_spec, (const float2*)dry_spec,
                                                             src_of, J, K, (long)Fc);
   return launched("mix_spectra_kernel");
 }
 
 int frir_mix_powers(const float* y, int64_t F, const int64_t* req_row, const int32_t* req_lo,
-                    const int32_t* req_hi, int32_t n_req, double* out, void* stream) {
-  if (!y || !req_row || !req_lo || !req_hi || !out || n_req < 0 || F < 1) {
+                    const int32_t* req_hi, int32_t n_req, double* scratch, double* out, void* stream) {
+  if (!y || !req_row || !req_lo || !req_hi || !scratch || !out || n_req < 0 || F < 1) {
     set_error("frir_mix_powers: invalid argument");
     return FRIR_EINVAL;
   }
   if (n_req == 0) return FRIR_OK;
-  mix_power_kernel<<<n_req, 256, 0, (cudaStream_t)stream>>>(y, req_row, req_lo, req_hi, (long)F, out);
+  mix_power_kernel<<<dim3(kPowChunks, n_req), 256, 0, (cudaStream_t)stream>>>(y, req_row, req_lo, req_hi,
+                                                                             (long)F, scratch);
+  mix_power_finish_kernel<<<(n_req + 127) / 128, 128, 0, (cudaStream_t)stream>>>(scratch, req_lo, req_hi,
+                                                                                n_req, out);
   return launched("mix_power_kernel");
 }
 
@@ -172,7 +259,7 @@ int frir_mix_combine(const float* y, const double* gains, const int32_t* total, 
     return FRIR_EINVAL;
   }
   if (B == 0 || T == 0) return FRIR_OK;
-  dim3 grid(grid_for((long)M * T, 256) / (B > 8 ? 8 : 1) + 1, B);
+  dim3 grid((unsigned)std::min<long>((T + 1023) / 1024, 64), M, B);
   mix_combine_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(y, gains, total, S, M, (long)F, (long)T,
                                                             mixture, sources, early, noise);
   return launched("mix_combine_kernel");

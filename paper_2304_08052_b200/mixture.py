@@ -19,13 +19,14 @@ drop-in for one utterance with numpy in and out.
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass
+from dataclasses import dataclass, replace
 
 import numpy as np
 
 from . import _abi
 
-__all__ = ["MixtureSpec", "MixtureResult", "spatialize_and_mix", "mix_device", "fft_size"]
+__all__ = ["MixtureSpec", "CurriculumState", "MixtureResult", "curriculum_step", "sample_scene",
+           "scene_batch_jobs", "spatialize_and_mix", "mix_device", "fft_size"]
 
 
 def _check_range(name, rng):
@@ -66,6 +67,61 @@ class MixtureSpec:
             raise ValueError("sir_scope must be 'full' or 'overlap'")
 
 
+@dataclass(frozen=True)
+class CurriculumState:
+    """Epoch-indexed cap on the sampled decay range, in milliseconds (mixture.py:83-96)."""
+
+    epoch: int = 0
+    lower_ms: float = 50.0
+    upper_ms: float = 100.0
+    step_ms: float = 50.0
+    max_ms: float = 700.0
+
+    @property
+    def t60_bounds(self) -> tuple:
+        return self.lower_ms / 1000.0, self.upper_ms / 1000.0
+
+
+def curriculum_step(state: CurriculumState) -> CurriculumState:
+    """Advance one epoch: raise the upper bound by the step, capped (mixture.py:99-105)."""
+    return replace(state, epoch=state.epoch + 1, upper_ms=min(state.upper_ms + state.step_ms, state.max_ms))
+
+
+def sample_scene(spec: MixtureSpec, rng, curriculum: CurriculumState | None = None) -> tuple:
+    """One utterance's (Scene, SimParams), drawing from ``rng`` in the
+    reference's order (mixture.py:171-213): room (3 uniforms), T60, then per
+    speaker and the point noise (last) distance / azimuth / elevation, then
+    the simulation seed."""
+    from .scene import Scene, SimParams, linear_array
+
+    room = (rng.uniform(*spec.room_length), rng.uniform(*spec.room_width), rng.uniform(*spec.room_height))
+    lo, hi = curriculum.t60_bounds if curriculum is not None else spec.t60_range
+    t60 = rng.uniform(lo, hi)
+    placements = []
+    for _ in range(spec.n_speakers + 1):  # + point noise
+        placements.append((rng.uniform(*spec.speaker_distance), rng.uniform(0.0, 2.0 * np.pi),
+                           rng.uniform(*spec.elevation_range)))
+    scene = Scene(room_dims=room, mic_positions=linear_array(spec.mic_spacings), sources=placements)
+    params = SimParams(t60=t60, sample_rate=spec.sample_rate, num_images=spec.num_images,
+                       seed=int(rng.integers(2**63)))
+    return scene, params
+
+
+def scene_batch_jobs(scenes, params):
+    """One job table (one job per (scene, source), scenes in order) and the
+    concatenated mic rows, for rendering many utterances' RIRs in one launch."""
+    from .api import scene_jobs
+
+    jobs, mics, off = [], [], 0
+    for sc, pr in zip(scenes, params):
+        j, m = scene_jobs(pr, sc)
+        j["mic_off"] = off
+        off += len(m)
+        jobs.append(j)
+        mics.append(m)
+    return np.concatenate(jobs), np.concatenate(mics, axis=0)
+
+
 @dataclass
 class MixtureResult:
     mixture: np.ndarray          # (M, N)
@@ -93,8 +149,9 @@ def mix_device(dry, dry_len, offsets, noise, noise_len, rir_full, rir_early, rir
     dry (B, S, N) float32 with valid lengths dry_len (B, S); offsets (B, S)
     (offsets[:, 0] == 0); noise (B, Nn) with lengths noise_len (B,);
     rir_full (B, S + 1, M, R) float32 (the noise filter last) with valid
-    lengths rir_len (B,); rir_early (B, S, M, R) or None (then the full filter,
-    as the reference copies the full image); sir_db (B, max(S - 1, 1)) and
+    lengths rir_len (B,); rir_early (B, >= S, M, R) or None (then the full
+    filter, as the reference copies the full image) -- both may be strided
+    views over the render's padded output (per-item blocks contiguous); sir_db (B, max(S - 1, 1)) and
     snr_db (B,) in dB.  Integer/size arguments are host arrays.  Returns a dict
     of device tensors: mixture (B, M, T), sources and early (B, S, M, T), noise
     (B, M, T), gains (B, S + 1) [speaker gains then the noise gain], total (B,)
@@ -117,25 +174,34 @@ def mix_device(dry, dry_len, offsets, noise, noise_len, rir_full, rir_early, rir
     lib = _abi.lib()
     stream = torch.cuda.current_stream(dev).cuda_stream
 
-    # dry signals at their offsets, then the point noise tiled to the dry length (:316-319)
-    x = torch.zeros((B, S + 1, F), dtype=torch.float32, device=dev)
-    for b in range(B):
-        for k in range(S):
-            o, n = int(offsets[b, k]), int(dry_len[b, k])
-            x[b, k, o:o + n] = dry[b, k, :n]
-        dl = int(total[b] - rir_len[b] + 1)
-        nl = int(noise_len[b])
-        reps = -(-dl // nl)
-        x[b, S, :dl] = noise[b, :nl].repeat(reps)[:dl]
+    i32 = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32), device=dev)  # noqa: E731
+    dry = dry.contiguous()
+    noise = noise.contiguous()
+    # filters: each item's [S(+1)][M][R] block must be contiguous; items may be strided
+    if rir_full.stride()[1:] != (M * R, R, 1):
+        rir_full = rir_full.contiguous()
+    if rir_early is not None and (rir_early.shape[0] != B or rir_early.shape[1] < S
+                                  or rir_early.shape[2:] != (M, R)):
+        raise ValueError("rir_early must be (B, >= S, M, R) like rir_full")
+    if rir_early is not None and rir_early.stride()[1:] != (M * R, R, 1):
+        rir_early = rir_early.contiguous()
+    # dry signals at their offsets, then the point noise tiled to the dry length (:307-312)
+    dlen = total - rir_len + 1
+    x = torch.empty((B, S + 1, F), dtype=torch.float32, device=dev)
+    # (device copies held in locals: a temporary's memory could be reused before the launch)
+    off_d, len_d, nlen_d, dlen_d = i32(offsets), i32(dry_len), i32(noise_len), i32(dlen)
+    _abi.check(lib.frir_mix_pack_dry(dry.data_ptr(), dry.stride(0), dry.stride(1), noise.data_ptr(),
+                                     noise.stride(0), off_d.data_ptr(), len_d.data_ptr(), nlen_d.data_ptr(),
+                                     dlen_d.data_ptr(), B, S, F, x.data_ptr(), stream), "frir_mix_pack_dry")
     # filter rows: kM+m full of speaker k, (S+k)M+m early, 2SM+m noise
     J = (2 * S + 1) * M
-    h = torch.zeros((B, J, F), dtype=torch.float32, device=dev)
-    for b in range(B):
-        r = int(rir_len[b])
-        h[b, :S * M, :r] = rir_full[b, :S, :, :r].reshape(S * M, r)
-        src_e = rir_early[b, :, :, :r] if rir_early is not None else rir_full[b, :S, :, :r]
-        h[b, S * M:2 * S * M, :r] = src_e.reshape(S * M, r)
-        h[b, 2 * S * M:, :r] = rir_full[b, S, :, :r]
+    h = torch.empty((B, J, F), dtype=torch.float32, device=dev)
+    rl = i32(rir_len)
+    _abi.check(lib.frir_mix_pack_filters(rir_full.data_ptr(), rir_full.stride(0),
+                                         rir_early.data_ptr() if rir_early is not None else None,
+                                         rir_early.stride(0) if rir_early is not None else 0,
+                                         rl.data_ptr(), B, S, M, R, F, h.data_ptr(), stream),
+               "frir_mix_pack_filters")
     src_of = torch.tensor(np.concatenate([np.repeat(np.arange(S), M), np.repeat(np.arange(S), M),
                                           np.full(M, S)]).astype(np.int32), device=dev)
     X = torch.fft.rfft(x, n=F)
@@ -146,27 +212,31 @@ def mix_device(dry, dry_len, offsets, noise, noise_len, rir_full, rir_early, rir
     y = torch.fft.irfft(H, n=F)
     del H, X
 
-    # reference-channel power requests (mixture.py:284-303, 311)
-    rows, lo, hi = [], [], []
-    for b in range(B):
-        base = b * J
-        tot = int(total[b])
-        rows.append(base); lo.append(0); hi.append(tot)                       # p_ref
-        for k in range(1, S):
-            if sir_scope == "overlap":
-                a = int(offsets[b, k])
-                e = min(tot, int(offsets[b, k] + dry_len[b, k] + rir_len[b] - 1))
-            else:
-                a, e = 0, tot
-            rows.append(base + k * M); lo.append(a); hi.append(e)           # p_int
-            rows.append(base); lo.append(a); hi.append(e)                   # p_tgt
-        rows.append(base + 2 * S * M); lo.append(0); hi.append(tot)       # p_noise
-    req_row = torch.tensor(rows, dtype=torch.int64, device=dev)
-    req_lo = torch.tensor(lo, dtype=torch.int32, device=dev)
-    req_hi = torch.tensor(hi, dtype=torch.int32, device=dev)
+    # reference-channel power requests (mixture.py:284-303, 311), per item:
+    # p_ref, (p_int_k, p_tgt_k) for k = 1..S-1, p_noise
+    base = np.arange(B, dtype=np.int64) * J
+    rows = np.empty((B, 2 * S), dtype=np.int64)
+    lo = np.zeros((B, 2 * S), dtype=np.int64)
+    hi = np.repeat(total[:, None], 2 * S, axis=1).astype(np.int64)
+    rows[:, 0] = base
+    rows[:, 2 * S - 1] = base + 2 * S * M
+    for k in range(1, S):
+        rows[:, 2 * k - 1] = base + k * M
+        rows[:, 2 * k] = base
+        if sir_scope == "overlap":
+            a = offsets[:, k]
+            e = np.minimum(total, offsets[:, k] + dry_len[:, k] + rir_len - 1)
+            lo[:, 2 * k - 1] = lo[:, 2 * k] = a
+            hi[:, 2 * k - 1] = hi[:, 2 * k] = e
+    rows, lo, hi = rows.ravel(), lo.ravel(), hi.ravel()
+    req_row = torch.as_tensor(rows, device=dev)
+    req_lo = i32(lo)
+    req_hi = i32(hi)
     pw = torch.empty(len(rows), dtype=torch.float64, device=dev)
+    scratch = torch.empty(len(rows) * _abi.MIX_POWER_CHUNKS, dtype=torch.float64, device=dev)
     _abi.check(lib.frir_mix_powers(y.data_ptr(), F, req_row.data_ptr(), req_lo.data_ptr(),
-                                   req_hi.data_ptr(), len(rows), pw.data_ptr(), stream), "frir_mix_powers")
+                                   req_hi.data_ptr(), len(rows), scratch.data_ptr(), pw.data_ptr(), stream),
+               "frir_mix_powers")
     sir = torch.as_tensor(np.asarray(sir_db, dtype=np.float64).reshape(B, max(S - 1, 1)), device=dev)
     snr = torch.as_tensor(np.asarray(snr_db, dtype=np.float64).reshape(B), device=dev)
     gains = torch.empty((B, S + 1), dtype=torch.float64, device=dev)

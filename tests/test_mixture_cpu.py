@@ -54,3 +54,20 @@ def test_short_source_rejected_before_compute():
                               offsets=[0, 7800])
     with pytest.raises(ValueError, match="one RIR"):
         MX.spatialize_and_mix([np.zeros(100)], np.zeros(100), [None] * 3, spec, rng)
+
+
+def test_sample_scene_matches_reference():
+    """Same draws, order and types as framrir.mixture.sample_scene (golden KAT)."""
+    import json
+    from pathlib import Path
+
+    kat = json.loads((Path(__file__).parent / "golden" / "scene_kat.json").read_text())
+    cur = MX.curriculum_step(MX.curriculum_step(MX.CurriculumState()))
+    assert [cur.upper_ms, cur.epoch] == kat["curriculum_upper_ms"]
+    for c in kat["cases"]:
+        rng = np.random.default_rng(c["seed"])
+        sc, pr = MX.sample_scene(MX.MixtureSpec(n_speakers=c["n_speakers"]), rng, cur if c["curriculum"] else None)
+        assert list(sc.room_dims) == c["room"] and pr.t60 == c["t60"] and pr.seed == c["sim_seed"]
+        assert np.asarray(sc.sources).tolist() == c["sources"]
+        assert np.asarray(sc.mic_positions).tolist() == c["mics"]
+        assert float(rng.random()) == c["next_u"]  # same number of draws consumed

@@ -234,15 +234,34 @@ def mix_cases():
     (OUT / "mix.json").write_text(json.dumps(meta, indent=1))
 
 
+def scene_kat():
+    """framrir.mixture.sample_scene draws (plus a curriculum-capped one)."""
+    from framrir.mixture import CurriculumState, MixtureSpec, curriculum_step, sample_scene
+
+    out = []
+    cur = curriculum_step(curriculum_step(CurriculumState()))
+    for seed in range(6):
+        rng = np.random.default_rng(seed)
+        spec = MixtureSpec(n_speakers=1 + seed % 3)
+        sc, pr = sample_scene(spec, rng, cur if seed % 2 else None)
+        out.append({"seed": seed, "n_speakers": spec.n_speakers, "curriculum": bool(seed % 2),
+                    "room": list(sc.room_dims), "t60": pr.t60, "sim_seed": int(pr.seed),
+                    "sources": np.asarray(sc.sources).tolist(),
+                    "mics": np.asarray(sc.mic_positions).tolist(), "next_u": float(rng.random())})
+    return {"cases": out, "curriculum_upper_ms": [cur.upper_ms, cur.epoch]}
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
     if "--mix-only" in sys.argv:
         mix_cases()
+        (OUT / "scene_kat.json").write_text(json.dumps(scene_kat(), indent=1))
         return
     (OUT / "kat.json").write_text(json.dumps(kat(), indent=1))
     cfg1()
     cases()
     mix_cases()
+    (OUT / "scene_kat.json").write_text(json.dumps(scene_kat(), indent=1))
     for f in sorted(OUT.iterdir()):
         print(f.name, f.stat().st_size)
 
