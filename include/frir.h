@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define FRIR_ABI_VERSION 1
+#define FRIR_ABI_VERSION 2
 
 enum {
   FRIR_OK = 0,
@@ -96,8 +96,12 @@ typedef struct {
   /* ---- extensions (defaults reproduce the reference) ---- */
   int32_t n_images_hi;       /* > n_images: I ~ U{n_images..n_images_hi} from stream (seed, k, 2) */
   int32_t normalize;         /* 0: reference scaling; 1: direct path of every channel = 1/1 m (x D_0m) */
+  int32_t kind;              /* FRIR_KIND_FRAM (0) or FRIR_KIND_ISM (1), see below */
+  int32_t pad2_;
   double early_lo_ms;        /* early window [-lo, +hi] ms around the direct path; 0/0 means 6/50 */
   double early_hi_ms;
+  double duration;           /* ISM: train length in s (0: t60), ism.py:39-60 */
+  double reflection;         /* ISM: reflection coefficient override (0: Eyring from room, t60) */
   /* ---- layout (frir_jobs_prepare) ---- */
   int64_t img_off;           /* first image row (row 0 = direct path) */
   int64_t item_off;          /* first (image, mic) item */
@@ -115,6 +119,15 @@ typedef struct {
   int32_t e_lo, e_hi;        /* early window in high-rate samples (core.py:257-258) */
   uint64_t key[4];          /* Philox keys of streams (seed, k, 0) and (seed, k, 1) */
 } frir_job;
+
+/* Job kinds.  FRIR_KIND_ISM runs the shoebox image-source reference
+   (ism.py:81-147, ism_rir) through the same chain: the images are given as
+   batch draws (draw_dist, draw_az, draw_el = ABSOLUTE x, y, z of image i,
+   draw_refl = its integer reflection count g), row 0 is the source itself at
+   `center` (d0 = 0), gains are r^g / D with r = exp(-0.0805 V/S/t60)
+   (ism.py:63-78) unless `reflection` > 0, and arrivals past the train end are
+   dropped instead of clamped (ism.py:131-133).  Full variant only. */
+enum { FRIR_KIND_FRAM = 0, FRIR_KIND_ISM = 1 };
 
 typedef struct {
   const frir_job* jobs;      /* device, n_jobs entries */

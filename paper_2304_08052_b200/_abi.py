@@ -45,8 +45,9 @@ class FrirJob(ctypes.Structure):
         ("beta", c_double), ("perturb_lo", c_double), ("perturb_hi", c_double), ("tau", c_double),
         ("seed", c_uint64), ("source_index", c_int32), ("n_images", c_int32),
         ("mic_off", c_int32), ("n_mics", c_int32),
-        ("n_images_hi", c_int32), ("normalize", c_int32),
-        ("early_lo_ms", c_double), ("early_hi_ms", c_double),
+        ("n_images_hi", c_int32), ("normalize", c_int32), ("kind", c_int32), ("pad2_", c_int32),
+        ("early_lo_ms", c_double), ("early_hi_ms", c_double), ("duration", c_double),
+        ("reflection", c_double),
         ("img_off", c_int64), ("item_off", c_int64), ("out_off", c_int64),
         ("chan_off", c_int32), ("out_stride", c_int32), ("L", c_int32), ("n1", c_int32),
         ("n2", c_int32), ("pad_", c_int32),
@@ -71,6 +72,8 @@ JOB_DTYPE = np.dtype(FrirJob)
 
 # (name, restype, argtypes) of every symbol include/frir.h declares.
 MIX_POWER_CHUNKS = 32  # FRIR_MIX_POWER_CHUNKS
+ABI_VERSION = 2  # FRIR_ABI_VERSION
+KIND_FRAM, KIND_ISM = 0, 1  # FRIR_KIND_*
 
 SIGNATURES = [
     ("frir_plan_create", c_int32, [c_int32, ctypes.POINTER(c_void_p)]),
@@ -130,7 +133,7 @@ def lib():
         fn = getattr(handle, name)
         fn.restype = restype
         fn.argtypes = argtypes
-    if handle.frir_abi_version() != 1:
+    if handle.frir_abi_version() != ABI_VERSION:
         raise FrirLibraryError("libfrir ABI version mismatch")
     for which, ty in ((0, FrirJob), (1, FrirBatch), (2, FrirPlanDesc)):
         if handle.frir_struct_size(which) != ctypes.sizeof(ty):

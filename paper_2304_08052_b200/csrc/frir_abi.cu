@@ -215,53 +215,81 @@ int frir_jobs_prepare(int32_t sample_rate, frir_job* jobs, int32_t n_jobs, int32
   for (int32_t j = 0; j < n_jobs; ++j) {
     frir_job& J = jobs[j];
     std::string pre = "job " + std::to_string(j) + ": ";
-    // extension: I ~ U{n_images .. n_images_hi} from the job's own stream (seed, k, 2)
-    if (J.n_images_hi > J.n_images && J.n_images >= 0) {
-      uint64_t k2[2];
-      seed_keys(J.seed, (uint64_t)J.source_index, 2, k2);
-      const double u = u64_to_unit(stream_word(k2, 0));
-      J.n_images += (int32_t)(u * (double)(J.n_images_hi - J.n_images + 1));
-      J.n_images_hi = J.n_images;  // idempotent: a prepared table keeps its draw
-    }
-    // SimParams.__post_init__ (params.py:49-65)
-    if (!(J.t60 > 0)) { set_error(pre + "t60 must be > 0, got " + fmt("%g", J.t60)); return FRIR_EINVAL; }
-    if (J.n_images < 0) { set_error(pre + "num_images must be >= 0"); return FRIR_EINVAL; }
-    if (!(0.0 <= J.alpha && J.alpha < J.beta && J.beta <= 1.0)) {
-      set_error(pre + "need 0 <= alpha < beta <= 1, got alpha=" + fmt("%g", J.alpha) + " beta=" + fmt("%g", J.beta));
+    if (J.kind != FRIR_KIND_FRAM && J.kind != FRIR_KIND_ISM) {
+      set_error(pre + "unknown job kind " + std::to_string(J.kind));
       return FRIR_EINVAL;
     }
-    if (J.perturb_lo > J.perturb_hi) { set_error(pre + "perturb_lo must be <= perturb_hi"); return FRIR_EINVAL; }
-    if (!(J.tau > 0)) { set_error(pre + "tau must be > 0, got " + fmt("%g", J.tau)); return FRIR_EINVAL; }
-    if (!(J.c0 > 0)) { set_error(pre + "sound_speed must be > 0"); return FRIR_EINVAL; }
-    // Scene (params.py:82-93)
-    for (int k = 0; k < 3; ++k)
-      if (!(J.room[k] > 0)) { set_error(pre + "room_dims must be 3 positive lengths"); return FRIR_EINVAL; }
-    if (J.n_mics < 1) { set_error(pre + "mic_positions must be an (M, 3) array with M >= 1"); return FRIR_EINVAL; }
-    if (!(J.d0 > 0)) { set_error(pre + "source distances must be > 0"); return FRIR_EINVAL; }
-    // reflection_coefficient (core.py:113-128)
-    double lx = J.room[0], ly = J.room[1], lz = J.room[2];
-    double volume = lx * ly * lz;
-    double surface = 2.0 * (lx * ly + lx * lz + ly * lz);
-    double ratio = volume / surface;
-    double t = 1.0 - std::exp(-0.16 * ratio / J.t60);
-    J.r = std::sqrt(1.0 - t * t);
-    // sample_image_geometry (core.py:140-148)
-    if (J.alpha == 0.0) { set_error(pre + "alpha must be > 0 to sample image distances"); return FRIR_EINVAL; }
-    double c_max = J.c0 * J.t60;
-    if (c_max <= J.d0) {
-      set_error(pre + "c0*t60 = " + fmt("%.3f", c_max) + " m must exceed the direct distance " + fmt("%.3f", J.d0) + " m");
-      return FRIR_EINVAL;
-    }
-    J.rr_max = 0.0;
-    if (J.n_images > 0) {  // core.py:295-299
+    const bool ism = J.kind == FRIR_KIND_ISM;
+    if (ism) {
+      // IsmConfig / ism_rir (ism.py:39-60, 63-78, 118-126); positions come as draws
+      if (!(J.t60 > 0)) { set_error(pre + "t60 must be > 0"); return FRIR_EINVAL; }
+      if (!(J.c0 > 0)) { set_error(pre + "sound_speed must be > 0"); return FRIR_EINVAL; }
+      for (int k = 0; k < 3; ++k)
+        if (!(J.room[k] > 0)) { set_error(pre + "room_dims must be 3 positive lengths"); return FRIR_EINVAL; }
+      if (J.n_mics < 1) { set_error(pre + "mic_positions must be an (M, 3) array with M >= 1"); return FRIR_EINVAL; }
+      if (J.n_images < 0 || J.n_images_hi > J.n_images) { set_error(pre + "image count must be >= 0"); return FRIR_EINVAL; }
+      if (!(J.duration >= 0) || !(J.reflection >= 0)) {
+        set_error(pre + "duration and reflection must be >= 0 (0 = default)");
+        return FRIR_EINVAL;
+      }
+      if (J.normalize != 0) { set_error(pre + "normalize is not defined for ISM jobs"); return FRIR_EINVAL; }
+      const double lx = J.room[0], ly = J.room[1], lz = J.room[2];
+      const double ratio = (lx * ly * lz) / (2.0 * (lx * ly + lx * lz + ly * lz));
+      J.r = J.reflection > 0 ? J.reflection : std::exp(-0.0805 * ratio / J.t60);
       if (!(0.0 < J.r && J.r < 1.0)) {
         set_error(pre + "reflection coefficient must be in (0, 1), got " + fmt("%.17g", J.r));
         return FRIR_EINVAL;
       }
-      J.rr_max = (std::log10(J.c0 * J.t60) - std::log10(J.d0) - 3.0) / std::log10(J.r);
-      if (J.rr_max < 1.0) {
-        set_error(pre + "rr_max must be >= 1, got " + fmt("%.17g", J.rr_max));
+      J.rr_max = 0.0;
+    } else {
+      // extension: I ~ U{n_images .. n_images_hi} from the job's own stream (seed, k, 2)
+      if (J.n_images_hi > J.n_images && J.n_images >= 0) {
+        uint64_t k2[2];
+        seed_keys(J.seed, (uint64_t)J.source_index, 2, k2);
+        const double u = u64_to_unit(stream_word(k2, 0));
+        J.n_images += (int32_t)(u * (double)(J.n_images_hi - J.n_images + 1));
+        J.n_images_hi = J.n_images;  // idempotent: a prepared table keeps its draw
+      }
+      // SimParams.__post_init__ (params.py:49-65)
+      if (!(J.t60 > 0)) { set_error(pre + "t60 must be > 0, got " + fmt("%g", J.t60)); return FRIR_EINVAL; }
+      if (J.n_images < 0) { set_error(pre + "num_images must be >= 0"); return FRIR_EINVAL; }
+      if (!(0.0 <= J.alpha && J.alpha < J.beta && J.beta <= 1.0)) {
+        set_error(pre + "need 0 <= alpha < beta <= 1, got alpha=" + fmt("%g", J.alpha) + " beta=" + fmt("%g", J.beta));
         return FRIR_EINVAL;
+      }
+      if (J.perturb_lo > J.perturb_hi) { set_error(pre + "perturb_lo must be <= perturb_hi"); return FRIR_EINVAL; }
+      if (!(J.tau > 0)) { set_error(pre + "tau must be > 0, got " + fmt("%g", J.tau)); return FRIR_EINVAL; }
+      if (!(J.c0 > 0)) { set_error(pre + "sound_speed must be > 0"); return FRIR_EINVAL; }
+      // Scene (params.py:82-93)
+      for (int k = 0; k < 3; ++k)
+        if (!(J.room[k] > 0)) { set_error(pre + "room_dims must be 3 positive lengths"); return FRIR_EINVAL; }
+      if (J.n_mics < 1) { set_error(pre + "mic_positions must be an (M, 3) array with M >= 1"); return FRIR_EINVAL; }
+      if (!(J.d0 > 0)) { set_error(pre + "source distances must be > 0"); return FRIR_EINVAL; }
+      // reflection_coefficient (core.py:113-128)
+      double lx = J.room[0], ly = J.room[1], lz = J.room[2];
+      double volume = lx * ly * lz;
+      double surface = 2.0 * (lx * ly + lx * lz + ly * lz);
+      double ratio = volume / surface;
+      double t = 1.0 - std::exp(-0.16 * ratio / J.t60);
+      J.r = std::sqrt(1.0 - t * t);
+      // sample_image_geometry (core.py:140-148)
+      if (J.alpha == 0.0) { set_error(pre + "alpha must be > 0 to sample image distances"); return FRIR_EINVAL; }
+      double c_max = J.c0 * J.t60;
+      if (c_max <= J.d0) {
+        set_error(pre + "c0*t60 = " + fmt("%.3f", c_max) + " m must exceed the direct distance " + fmt("%.3f", J.d0) + " m");
+        return FRIR_EINVAL;
+      }
+      J.rr_max = 0.0;
+      if (J.n_images > 0) {  // core.py:295-299
+        if (!(0.0 < J.r && J.r < 1.0)) {
+          set_error(pre + "reflection coefficient must be in (0, 1), got " + fmt("%.17g", J.r));
+          return FRIR_EINVAL;
+        }
+        J.rr_max = (std::log10(J.c0 * J.t60) - std::log10(J.d0) - 3.0) / std::log10(J.r);
+        if (J.rr_max < 1.0) {
+          set_error(pre + "rr_max must be >= 1, got " + fmt("%.17g", J.rr_max));
+          return FRIR_EINVAL;
+        }
       }
     }
     J.log2r = std::log2(J.r);
@@ -286,7 +314,7 @@ int frir_jobs_prepare(int32_t sample_rate, frir_job* jobs, int32_t n_jobs, int32
     seed_keys(J.seed, (uint64_t)J.source_index, 1, key);
     J.key[2] = key[0]; J.key[3] = key[1];
     // lengths (core.py:239, scipy resample_poly output lengths)
-    double Ld = std::ceil(J.t60 * (double)rate);
+    double Ld = std::ceil((ism && J.duration > 0 ? J.duration : J.t60) * (double)rate);
     if (!(Ld >= 1.0 && Ld < 2.0e9)) { set_error(pre + "RIR length out of range"); return FRIR_ERANGE; }
     J.L = (int32_t)Ld;
     int64_t n1 = ceil_div64((int64_t)J.L * d.up, d.down);

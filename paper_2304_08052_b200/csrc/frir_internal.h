@@ -19,7 +19,7 @@ constexpr int kChunk = kTile / 32;  // serial outputs per lane in the scan
 // with output windows so the scan can store float4s.
 constexpr int kExt = 32;
 constexpr int kSpBias = 64;     // bias of the packed start index
-constexpr int kMaxRows = 17408; // max images + 1 per job (K2 block sort capacity)
+constexpr int kMaxRows = 1 << 22;  // max images + 1 per job (item index arithmetic)
 constexpr int kLtMax = 128;     // max stage-1 taps past n1 (lt_max = (half1 - up) / down + 2, 91 at 11025 Hz)
 // Per-warp row length of the render kernel's past-n1 tap sums, sized per rate
 // so the 16 kHz plan keeps two CTAs per SM.

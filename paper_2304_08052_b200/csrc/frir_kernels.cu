@@ -141,13 +141,19 @@ __global__ void __launch_bounds__(128, 8) geom_kernel(GeomArgs A) {
   const double* mics = A.mics + 3 * (size_t)J.mic_off;
   const double rate_c0 = __ddiv_rn(A.rate, J.c0);
   int2* items = A.ws.items_raw + J.item_off;
+  const int ism = J.kind == FRIR_KIND_ISM;  // 1: arrivals past L - 1 are dropped, not clamped
   if (g == 0) {  // row 0: direct path (core.py:169, params.py:156-159), r**0 = 1
     double x, y, z;
     image_position(J, J.d0, J.az, J.el, &x, &y, &z);
     for (int m = 0; m < M; ++m) {
       double D;
-      int q = delay_of(x, y, z, mics + 3 * m, J.c0, A.rate, rate_c0, J.L, &D);
-      items[(size_t)m * rows] = make_item(q, (float)__drcp_rn(D), A.r_h, A.t0, A.rh_magic);
+      int q = delay_of(x, y, z, mics + 3 * m, J.c0, A.rate, rate_c0, J.L + ism, &D);
+      // ISM drops arrivals past the train end (ism.py:131-133): gain 0 at a
+      // neutral mid-train position; the direct index still clamps (:134-136)
+      const bool drop = q > J.L - 1;
+      q = min(q, J.L - 1);
+      items[(size_t)m * rows] = make_item(drop ? J.L / 2 : q, drop ? 0.f : (float)__drcp_rn(D), A.r_h, A.t0,
+                                          A.rh_magic);
       A.ws.chan_q0[J.chan_off + m] = q;
       A.ws.chan_scale[J.chan_off + m] = J.normalize ? (float)D : 1.0f;  // direct path -> 1/(1 m)
       // resample.py:115-119: clip(round(q0 / r_h), 0, n2 - 1), half-even
@@ -210,7 +216,11 @@ __global__ void __launch_bounds__(128, 8) geom_kernel(GeomArgs A) {
   float lg[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    image_position(J, dist[k], th[k], ph[k], &px[k], &py[k], &pz[k]);
+    if (J.kind == FRIR_KIND_ISM) {  // lattice images arrive as absolute positions
+      px[k] = dist[k]; py[k] = th[k]; pz[k] = ph[k];
+    } else {
+      image_position(J, dist[k], th[k], ph[k], &px[k], &py[k], &pz[k]);
+    }
     // core.py:246 r ** g; the gain is an FP32 quantity (exp2 of an FP64 exponent)
     const double x = refl[k] * J.log2r, xi = floor(x);
     lg[k] = ldexpf(exp2f((float)(x - xi)), (int)xi);
@@ -223,7 +233,11 @@ __global__ void __launch_bounds__(128, 8) geom_kernel(GeomArgs A) {
     for (int k = 0; k < 4; ++k) {
       if (k < nk) {
         double D;
-        int q = delay_of(px[k], py[k], pz[k], mics + 3 * m, J.c0, A.rate, rate_c0, J.L, &D);
+        const int q = delay_of(px[k], py[k], pz[k], mics + 3 * m, J.c0, A.rate, rate_c0, J.L + ism, &D);
+        if (q > J.L - 1) {  // ISM only: dropped arrival
+          out[k] = make_item(J.L / 2, 0.f, A.r_h, A.t0, A.rh_magic);
+          continue;
+        }
         FRIR_CHECK(q >= 0 && q < J.L && r0 + k < rows);
         out[k] = make_item(q, lg[k] / (float)D, A.r_h, A.t0, A.rh_magic);
       }
@@ -265,6 +279,16 @@ constexpr int kSortWarps = kSortThreads / 32;
 // one exclusive scan in (bucket, warp) order, then a stable scatter into the
 // sorted buffer.  Only the counters live in smem, so long channels keep the
 // SM occupied.
+// Counter type CT: 16-bit (packed pairs) while rows <= 65535, else 32-bit.
+template <typename CT>
+__device__ __forceinline__ void count_add(CT* cnt, int idx) {
+  if constexpr (sizeof(CT) == 2)
+    atomicAdd(reinterpret_cast<unsigned*>(cnt) + (idx >> 1), 1u << (16 * (idx & 1)));
+  else
+    atomicAdd(reinterpret_cast<unsigned*>(cnt) + idx, 1u);
+}
+
+template <typename CT>
 __global__ void __launch_bounds__(kSortThreads) sort_kernel(SortArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_wsum[kSortWarps];
@@ -277,10 +301,11 @@ __global__ void __launch_bounds__(kSortThreads) sort_kernel(SortArgs A) {
   const size_t base = J.item_off + (size_t)m * rows;
   const int2* src = A.ws.items_raw + base;
   int2* dst = A.ws.items + base;
-  unsigned short* s_cnt = reinterpret_cast<unsigned short*>(smem);  // [nbk][warps]
+  CT* s_cnt = reinterpret_cast<CT*>(smem);  // [nbk][warps]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = nbk * kSortWarps;
-  for (int i = tid; i < (n + 1) / 2; i += kSortThreads) reinterpret_cast<unsigned*>(s_cnt)[i] = 0u;
+  const int nwords = (int)((n * sizeof(CT) + 3) / 4);
+  for (int i = tid; i < nwords; i += kSortThreads) reinterpret_cast<unsigned*>(s_cnt)[i] = 0u;
   __syncthreads();
   // pass 1: per-warp histograms over a contiguous row chunk per warp
   const int chunk = (rows + kSortWarps - 1) / kSortWarps;
@@ -288,8 +313,7 @@ __global__ void __launch_bounds__(kSortThreads) sort_kernel(SortArgs A) {
 #pragma unroll 4
   for (int r = r_lo + lane; r < r_hi; r += 32) {
     const int b = (__ldg(&src[r].x) & 0xFFFFF) >> 5;
-    atomicAdd(reinterpret_cast<unsigned*>(s_cnt) + ((b * kSortWarps + warp) >> 1),
-              1u << (16 * ((b * kSortWarps + warp) & 1)));
+    count_add(s_cnt, b * kSortWarps + warp);
   }
   __syncthreads();
   // exclusive scan over (bucket, warp) in bucket-major order: serial per
@@ -310,7 +334,7 @@ __global__ void __launch_bounds__(kSortThreads) sort_kernel(SortArgs A) {
   for (int w2 = 0; w2 < warp; ++w2) run += s_wsum[w2];
   for (int i = lo; i < hi; ++i) {
     const int cnt = s_cnt[i];
-    s_cnt[i] = (unsigned short)run;
+    s_cnt[i] = (CT)run;
     run += cnt;
   }
   __syncthreads();
@@ -337,13 +361,13 @@ __global__ void __launch_bounds__(kSortThreads) sort_kernel(SortArgs A) {
       peers &= bit ? ones : ~ones;
     }
     const int rank = __popc(peers & ((1u << lane) - 1u));
-    unsigned short* slot = s_cnt + (ok ? b * kSortWarps + warp : 0);
+    CT* slot = s_cnt + (ok ? b * kSortWarps + warp : 0);
     const int pos = ok ? *slot + rank : 0;
     FRIR_CHECK(!ok || (pos >= 0 && pos < rows && b < nbk));
     __syncwarp();
     if (ok) {
       dst[pos] = it;
-      if (rank == 0) *slot = (unsigned short)(*slot + __popc(peers));
+      if (rank == 0) *slot = (CT)(*slot + __popc(peers));
     }
     __syncwarp();
   }
@@ -995,11 +1019,12 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_
     sa.jobs = b->jobs; sa.chan_job = b->chan_job; sa.ws = ws;
     sa.r_h = d.r_h; sa.t0 = d.t0; sa.plan = plan->dev;
     const int nbk = ((b->max_windows * kWin + kSpBias) >> 5) + 3;
-    size_t smem = align16((size_t)nbk * kSortWarps * 2) +
-                  (size_t)(kSortWarps + 1) * 2 * lt_cap(d) * 8 + kSortWarps * 32;
-    e = cudaFuncSetAttribute(sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const bool wide = b->max_rows > 65535;  // sorted positions need 32-bit counters
+    const size_t smem = align16((size_t)nbk * kSortWarps * (wide ? 4 : 2));
+    auto kern = wide ? sort_kernel<uint32_t> : sort_kernel<uint16_t>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess) {
-      sort_kernel<<<b->total_channels, kSortThreads, smem, st>>>(sa);
+      kern<<<b->total_channels, kSortThreads, smem, st>>>(sa);
       e = cudaGetLastError();
     }
     if (e != cudaSuccess) { set_error(std::string("sort_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }

@@ -30,6 +30,8 @@ def golden():
         "cases_meta": json.loads((g / "cases.json").read_text()),
         "mix": dict(np.load(g / "mix.npz")),
         "mix_meta": json.loads((g / "mix.json").read_text()),
+        "ism": dict(np.load(g / "ism.npz")),
+        "ism_meta": json.loads((g / "ism.json").read_text()),
     }
 
 

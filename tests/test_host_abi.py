@@ -154,5 +154,25 @@ def test_jobs_prepare_rejects_like_reference(kw, msg):
 
 
 def test_jobs_prepare_rejects_oversized_jobs():
-    with pytest.raises(_abi.FrirLibraryError):
-        engine.prepare(16000, _one_job(n_images=40000), MICS)
+    with pytest.raises(_abi.FrirLibraryError, match="exceeds the supported maximum"):
+        engine.prepare(16000, _one_job(n_images=1 << 22), MICS)
+    engine.prepare(16000, _one_job(n_images=100000), MICS)  # large (ISM-sized) lists are fine
+
+
+def test_jobs_prepare_ism_rules():
+    j = _one_job()
+    j["kind"] = _abi.KIND_ISM
+    j["d0"] = 0.0
+    j["duration"] = 0.05
+    pb = engine.prepare(16000, j, MICS)
+    assert pb.jobs[0]["L"] == int(np.ceil(0.05 * 62 * 16000))
+    r = pb.jobs[0]["r"]
+    lx, ly, lz = j["room"][0]
+    assert r == np.exp(-0.0805 * (lx * ly * lz) / (2.0 * (lx * ly + lx * lz + ly * lz)) / j["t60"][0])
+    j["reflection"] = 1.5
+    with pytest.raises(ValueError, match="reflection coefficient must be in"):
+        engine.prepare(16000, j, MICS)
+    j["reflection"] = 0.0
+    j["kind"] = 7
+    with pytest.raises(ValueError, match="unknown job kind"):
+        engine.prepare(16000, j, MICS)

@@ -16,6 +16,9 @@ reference.  Cases:
                       inputs (explicit and rng-drawn offsets/SIR/SNR, both
                       SIR scopes, 1-3 speakers, missing early filters, tiled
                       noise): inputs and reference outputs (float32).
+* scene_kat.json      framrir.mixture.sample_scene draws.
+* ism.npz / ism.json  framrir.ism.ism_rir outputs (float32) and metadata on
+                      small rooms.
 """
 
 from __future__ import annotations
@@ -251,8 +254,42 @@ def scene_kat():
     return {"cases": out, "curriculum_upper_ms": [cur.upper_ms, cur.epoch]}
 
 
+def ism_cases():
+    """framrir.ism.ism_rir on small rooms (explicit and default orders,
+    duration and reflection overrides, 16 and 48 kHz)."""
+    from framrir.ism import IsmConfig, ism_rir
+
+    specs = [
+        dict(room_dims=(4.0, 3.5, 2.6), source_position=(1.2, 2.0, 1.3),
+             mic_positions=[(2.5, 1.5, 1.2), (2.55, 1.5, 1.2)], t60=0.12, max_order=3),
+        dict(room_dims=(3.0, 3.2, 2.5), source_position=(0.8, 1.1, 1.4),
+             mic_positions=[(2.0, 2.1, 1.0), (2.0, 2.15, 1.0), (2.05, 2.1, 1.0)], t60=0.08),
+        dict(room_dims=(5.0, 4.0, 3.0), source_position=(3.9, 0.7, 2.2),
+             mic_positions=[(1.0, 3.0, 1.5)], t60=0.3, max_order=2, duration=0.05, reflection=0.85),
+        dict(room_dims=(4.0, 3.5, 2.6), source_position=(1.2, 2.0, 1.3),
+             mic_positions=[(2.5, 1.5, 1.2), (2.54, 1.5, 1.2)], t60=0.1, max_order=2, sample_rate=48000),
+        dict(room_dims=(6.0, 5.0, 3.0), source_position=(2.0, 3.5, 1.5),
+             mic_positions=[(2.925, 2.5, 1.2), (3.075, 2.5, 1.2)], t60=0.2, max_order=0),
+    ]
+    blobs, meta = {}, []
+    for i, kw in enumerate(specs):
+        out = ism_rir(IsmConfig(**kw))
+        blobs[f"c{i}_samples"] = out.samples.astype(np.float32)
+        blobs[f"c{i}_direct"] = out.direct_path_sample
+        meta.append({"cfg": {k: (list(map(list, v)) if k == "mic_positions" else (list(v) if isinstance(v, tuple)
+                                                                                  else v)) for k, v in kw.items()},
+                     "peak": float(np.abs(out.samples).max()),
+                     "metadata": {k: (float(v) if isinstance(v, (np.floating,)) else v)
+                                  for k, v in out.metadata.items()}})
+    np.savez_compressed(OUT / "ism.npz", **blobs)
+    (OUT / "ism.json").write_text(json.dumps(meta, indent=1))
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
+    if "--ism-only" in sys.argv:
+        ism_cases()
+        return
     if "--mix-only" in sys.argv:
         mix_cases()
         (OUT / "scene_kat.json").write_text(json.dumps(scene_kat(), indent=1))
@@ -262,6 +299,7 @@ def main():
     cases()
     mix_cases()
     (OUT / "scene_kat.json").write_text(json.dumps(scene_kat(), indent=1))
+    ism_cases()
     for f in sorted(OUT.iterdir()):
         print(f.name, f.stat().st_size)
 
