@@ -245,6 +245,19 @@ int frir_mix_combine(const float* y, const double* gains, const int32_t* total, 
                      int32_t M, int64_t F, int64_t T, float* mixture, float* sources, float* early,
                      float* noise, void* stream);
 
+/* ---- batched decay measurement (decay.py:8-49) ----
+   Rows h[c][0:len[c]] (float32, row stride ld floats).  frir_edc writes the
+   unnormalised energy decay curve edc[c][i] = sum_{j>=i} h[c][j]^2 in FP64,
+   summed sequentially from the end exactly like numpy's cumsum of the
+   reversed squares (bit-identical), and amax[c] = max |h[c]|. */
+int frir_edc(const float* h, int64_t ld, const int32_t* len, int32_t C, double* edc, int64_t ld_out,
+             double* amax, void* stream);
+/* measure_t60 (decay.py:20-49) per row from frir_edc's outputs: NaN when the
+   row has no energy or less than min_drop dB of usable range. */
+int frir_t60(const float* h, int64_t ld, const int32_t* len, int32_t C, const double* edc, int64_t ld_e,
+             const double* amax, double sample_rate, double max_drop, double floor_margin, double min_drop,
+             double* t60, void* stream);
+
 const char* frir_last_error(void);
 int32_t frir_abi_version(void);
 /* Debug builds (-DFRIR_DEBUG): source line of the first failed in-kernel

@@ -32,7 +32,14 @@ def golden():
         "mix_meta": json.loads((g / "mix.json").read_text()),
         "ism": dict(np.load(g / "ism.npz")),
         "ism_meta": json.loads((g / "ism.json").read_text()),
+        "decay": dict(np.load(g / "decay.npz")),
+        "decay_meta": json.loads((g / "decay.json").read_text()),
     }
+
+
+@pytest.fixture(scope="session")
+def golden_dir():
+    return ROOT / "tests" / "golden"
 
 
 @pytest.fixture(scope="session", autouse=True)

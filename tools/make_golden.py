@@ -19,6 +19,9 @@ reference.  Cases:
 * scene_kat.json      framrir.mixture.sample_scene draws.
 * ism.npz / ism.json  framrir.ism.ism_rir outputs (float32) and metadata on
                       small rooms.
+* decay.npz / .json   framrir.decay.schroeder_curve / measure_t60 on float32
+                      rows (cfg 1 RIRs, exponential decays, edge cases).
+* container.frir      a framrir.io.write_rir_container file (2 records).
 """
 
 from __future__ import annotations
@@ -285,8 +288,54 @@ def ism_cases():
     (OUT / "ism.json").write_text(json.dumps(meta, indent=1))
 
 
+def decay_cases():
+    """framrir.decay on float32-representable rows: the cfg 1 reference RIRs,
+    exponential decays, leading silence, a short (NaN) tail."""
+    from framrir.decay import measure_t60, schroeder_curve
+
+    g = np.load(OUT / "cfg1.npz")
+    rows = [g["full"][m].astype(np.float64) for m in range(g["full"].shape[0])]
+    rows += [g["early"][0].astype(np.float64)]
+    rng = np.random.default_rng(3)
+    for t60 in (0.2, 0.5, 0.9):
+        n = int(1.2 * t60 * 16000)
+        env = 10.0 ** (-3.0 * np.arange(n) / (t60 * 16000))
+        rows.append((rng.standard_normal(n) * env).astype(np.float32).astype(np.float64))
+    sil = np.concatenate([np.zeros(300), rows[-1][:4000]])
+    rows.append(sil)
+    rows.append((rng.standard_normal(500) * 10.0 ** (-np.arange(500) / 400.0)).astype(np.float32).astype(np.float64))
+    out = {"t60": []}
+    blobs = {}
+    for i, r in enumerate(rows):
+        if i >= 5:  # rows 0-4 are cfg1.npz full[0..3], early[0]
+            blobs[f"r{i}"] = r.astype(np.float32)
+        out["t60"].append(measure_t60(r, 16000))
+        c = schroeder_curve(r)
+        idx = np.unique(np.linspace(0, len(c) - 1, 97).astype(np.int64))
+        blobs[f"edc_idx{i}"] = idx
+        blobs[f"edc{i}"] = c[idx]  # exact FP64 checkpoints of the normalised curve
+    np.savez_compressed(OUT / "decay.npz", **blobs)
+    (OUT / "decay.json").write_text(json.dumps({"t60": [None if math.isnan(x) else x for x in out["t60"]],
+                                                "n": len(rows)}, indent=1))
+
+
+def container_case():
+    """A small container written by framrir.io.write_rir_container."""
+    from framrir.io import RirRecord, write_rir_container
+
+    rng = np.random.default_rng(9)
+    recs = [RirRecord(samples=rng.standard_normal((2, 17)).astype(np.float32), sample_rate=16000, kind="full",
+                      seed=123),
+            RirRecord(samples=rng.standard_normal((3, 5)), sample_rate=48000, kind="early", seed=2**63 - 5)]
+    write_rir_container(OUT / "container.frir", recs)
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
+    if "--decay-only" in sys.argv:
+        decay_cases()
+        container_case()
+        return
     if "--ism-only" in sys.argv:
         ism_cases()
         return
@@ -300,6 +349,8 @@ def main():
     mix_cases()
     (OUT / "scene_kat.json").write_text(json.dumps(scene_kat(), indent=1))
     ism_cases()
+    decay_cases()
+    container_case()
     for f in sorted(OUT.iterdir()):
         print(f.name, f.stat().st_size)
 
