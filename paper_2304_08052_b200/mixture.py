@@ -25,8 +25,8 @@ import numpy as np
 
 from . import _abi
 
-__all__ = ["MixtureSpec", "CurriculumState", "MixtureResult", "curriculum_step", "sample_scene",
-           "scene_batch_jobs", "spatialize_and_mix", "mix_device", "fft_size"]
+__all__ = ["MixtureSpec", "CurriculumState", "MixtureResult", "SyntheticPool", "curriculum_step",
+           "sample_scene", "scene_batch_jobs", "spatialize_and_mix", "mix_device", "generate_batch", "fft_size"]
 
 
 def _check_range(name, rng):
@@ -85,6 +85,30 @@ class CurriculumState:
 def curriculum_step(state: CurriculumState) -> CurriculumState:
     """Advance one epoch: raise the upper bound by the step, capped (mixture.py:99-105)."""
     return replace(state, epoch=state.epoch + 1, upper_ms=min(state.upper_ms + state.step_ms, state.max_ms))
+
+
+@dataclass(frozen=True)
+class SyntheticPool:
+    """Self-contained source material: amplitude-modulated filtered noise
+    (mixture.py:116-139), drawn on the host from the caller's rng exactly as
+    the reference draws it (normals, leaky integrator, envelope phase)."""
+
+    lowpass_hz: float = 3800.0
+    modulation_hz: float = 3.0
+
+    def draw(self, rng, n_samples: int, sample_rate: int) -> np.ndarray:
+        from scipy.signal import lfilter
+
+        x = rng.standard_normal(n_samples)
+        a = math.exp(-2.0 * math.pi * self.lowpass_hz / sample_rate)
+        x = lfilter([1.0 - a], [1.0, -a], x)
+        x -= x.mean()
+        t = np.arange(n_samples) / sample_rate
+        phase = rng.uniform(0.0, 2.0 * np.pi)
+        envelope = 0.55 + 0.45 * np.sin(2.0 * np.pi * self.modulation_hz * t + phase)
+        x = x * envelope
+        peak = np.abs(x).max()
+        return x / peak if peak > 0 else x
 
 
 def sample_scene(spec: MixtureSpec, rng, curriculum: CurriculumState | None = None) -> tuple:
@@ -347,3 +371,90 @@ def spatialize_and_mix(sources: list, noise: np.ndarray, rirs: list, spec: Mixtu
             "overlap_ratios": overlap_ratios,
         },
     )
+
+
+def generate_batch(batch_size: int, spec: MixtureSpec, curriculum: CurriculumState | None = None, seed: int = 0,
+                   workers: int = 1, pool=None, executor=None, *, device=None) -> list:
+    """``batch_size`` independent utterances (drop-in for mixture.py:365-395).
+
+    Every random draw happens on the host in the reference's order from the
+    per-item stream Philox(SeedSequence((seed, index))) -- scene, dry sources
+    and noise, offsets, SIR, SNR -- so the content matches the reference item
+    for item.  All RIRs of the batch then render in ONE device launch (full +
+    early, (n_speakers + 1) sources per item) and are mixed on the device in
+    one ``mix_device`` call.  ``workers`` / ``executor`` are accepted for
+    signature compatibility; the device does the parallel work.
+    """
+    if batch_size < 0:
+        raise ValueError("batch_size must be >= 0")
+    if batch_size == 0:
+        return []
+    torch = _torch()
+    from . import engine
+
+    pool = SyntheticPool() if pool is None else pool
+    S = spec.n_speakers
+    fs = spec.sample_rate
+    n_dry = int(spec.utterance_seconds * spec.sample_rate)
+    scenes, params, dry, noises, offsets, sirs, snrs = [], [], [], [], [], [], []
+    for i in range(batch_size):  # mixture.py:335-342, then spatialize_and_mix's draws (:245-263)
+        rng = np.random.Generator(np.random.Philox(np.random.SeedSequence((int(seed), int(i)))))
+        sc, pr = sample_scene(spec, rng, curriculum)
+        srcs = [pool.draw(rng, n_dry, fs) for _ in range(S)]
+        nz = pool.draw(rng, n_dry, fs)
+        offs = _draw_offsets(srcs, spec, rng)
+        for k in range(1, S):
+            achieved = _overlap_ratio(len(srcs[0]), offs[k], len(srcs[k]))
+            if achieved < spec.min_overlap_ratio:
+                raise ValueError(f"speaker {k} overlap ratio {achieved:.2f} is below the "
+                                 f"required {spec.min_overlap_ratio}")
+        sirs.append([float(rng.uniform(*spec.sir_db)) for _ in range(S - 1)])
+        snrs.append(float(rng.uniform(*spec.snr_db)))
+        scenes.append(sc)
+        params.append(pr)
+        dry.append(np.stack([np.asarray(x, dtype=np.float32) for x in srcs]))
+        noises.append(np.asarray(nz, dtype=np.float32))
+        offsets.append(offs)
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    jobs, mics = scene_batch_jobs(scenes, params)
+    pb = engine.prepare(fs, jobs, mics, padded=True)
+    res = engine.DeviceBatch(pb, device=dev).run(include_early=True)
+    B = batch_size
+    M = len(scenes[0].mic_positions)
+    stride = int(pb.jobs[0]["out_stride"])
+    rir_len = pb.jobs["n2"].reshape(B, S + 1)[:, 0]
+    out = mix_device(torch.as_tensor(np.stack(dry), device=dev), [[n_dry] * S] * B, offsets,
+                     torch.as_tensor(np.stack(noises), device=dev), [n_dry] * B,
+                     res.full.view(B, S + 1, M, stride), res.early.view(B, S + 1, M, stride), rir_len,
+                     [x if S > 1 else [0.0] for x in sirs], snrs, sir_scope=spec.sir_scope)
+    mix_h = out["mixture"].cpu().numpy()
+    src_h = out["sources"].cpu().numpy()
+    early_h = out["early"].cpu().numpy()
+    noise_h = out["noise"].cpu().numpy()
+    gains = out["gains"].cpu().numpy()
+    results = []
+    for b in range(B):
+        T = int(out["total"][b])
+        md = {
+            "offsets": list(offsets[b]),
+            "gains": [float(g) for g in gains[b, :S]],
+            "noise_gain": float(gains[b, S]),
+            "sir_db": sirs[b],
+            "snr_db": snrs[b],
+            "overlap_ratios": [_overlap_ratio(n_dry, offsets[b][k], n_dry) for k in range(1, S)],
+            "index": b,
+            "seed": seed,
+            "sim_seed": params[b].seed,
+            "t60": params[b].t60,
+            "room_dims": list(scenes[b].room_dims),
+            "doas_deg": [float(np.degrees(x[1])) for x in np.atleast_2d(scenes[b].sources)],
+            "distances": [float(x[0]) for x in np.atleast_2d(scenes[b].sources)],
+        }
+        results.append(MixtureResult(
+            mixture=mix_h[b, :, :T].copy(),
+            sources=[src_h[b, k, :, :T].copy() for k in range(S)],
+            early_sources=[early_h[b, k, :, :T].copy() for k in range(S)],
+            noise=noise_h[b, :, :T].copy(),
+            metadata=md,
+        ))
+    return results

@@ -155,3 +155,29 @@ def test_with_rendered_rirs_vs_oracle_port():
     assert np.abs(res.mixture - mix).max() / pk < TOL
     assert np.abs(res.early_sources[1] - pe[1]).max() / pk < TOL
     assert np.allclose(md["gains"], gains, rtol=1e-5)
+
+
+def test_generate_batch_matches_reference(golden_dir):
+    """generate_batch end to end (host draws in the reference's order, RIRs
+    and mixing on the device) vs framrir.mixture.generate_batch."""
+    import json
+
+    from paper_2304_08052_b200 import mixture as MX
+
+    ref = dict(np.load(golden_dir / "genbatch.npz"))
+    meta = json.loads((golden_dir / "genbatch.json").read_text())
+    spec = MX.MixtureSpec(num_images=64, utterance_seconds=0.15, speaker_distance=(0.5, 2.0),
+                          room_length=(4.0, 6.0), room_width=(4.0, 6.0), t60_range=(0.1, 0.15))
+    res = MX.generate_batch(2, spec, seed=5)
+    for i, r in enumerate(res):
+        m = meta[i]
+        for k in ("offsets", "sir_db", "snr_db", "index", "seed", "sim_seed", "t60", "room_dims", "doas_deg",
+                  "distances", "overlap_ratios"):
+            assert r.metadata[k] == m[k], k
+        assert np.allclose(r.metadata["gains"], m["gains"], rtol=1e-5)
+        assert r.metadata["noise_gain"] == pytest.approx(m["noise_gain"], rel=1e-5)
+        pk = np.abs(ref[f"i{i}_mixture"]).max()
+        assert r.mixture.dtype == np.float32 or r.mixture.shape == ref[f"i{i}_mixture"].shape
+        assert np.abs(r.mixture - ref[f"i{i}_mixture"]).max() / pk < TOL
+    assert np.abs(res[0].sources[1] - ref["i0_src1"]).max() / np.abs(ref["i0_mixture"]).max() < TOL
+    assert np.abs(res[1].early_sources[0] - ref["i1_early0"]).max() / np.abs(ref["i1_mixture"]).max() < TOL

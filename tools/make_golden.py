@@ -22,6 +22,7 @@ reference.  Cases:
 * decay.npz / .json   framrir.decay.schroeder_curve / measure_t60 on float32
                       rows (cfg 1 RIRs, exponential decays, edge cases).
 * container.frir      a framrir.io.write_rir_container file (2 records).
+* genbatch.npz/.json  framrir.mixture.generate_batch (2 items, small spec).
 """
 
 from __future__ import annotations
@@ -330,8 +331,28 @@ def container_case():
     write_rir_container(OUT / "container.frir", recs)
 
 
+def generate_case():
+    """framrir.mixture.generate_batch on a small spec (2 items)."""
+    from framrir.mixture import MixtureSpec, generate_batch
+
+    spec = MixtureSpec(num_images=64, utterance_seconds=0.15, speaker_distance=(0.5, 2.0),
+                       room_length=(4.0, 6.0), room_width=(4.0, 6.0), t60_range=(0.1, 0.15))
+    res = generate_batch(2, spec, seed=5)
+    blobs, meta = {}, []
+    for i, r in enumerate(res):
+        blobs[f"i{i}_mixture"] = r.mixture
+        blobs[f"i{i}_" + ("src1" if i == 0 else "early0")] = r.sources[1] if i == 0 else r.early_sources[0]
+        meta.append({k: (list(map(float, v)) if isinstance(v, (list, tuple)) and k != "offsets" else
+                         (int(v) if isinstance(v, (np.integer,)) else v)) for k, v in r.metadata.items()})
+    np.savez_compressed(OUT / "genbatch.npz", **blobs)
+    (OUT / "genbatch.json").write_text(json.dumps(meta, indent=1, default=float))
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
+    if "--gen-only" in sys.argv:
+        generate_case()
+        return
     if "--decay-only" in sys.argv:
         decay_cases()
         container_case()
@@ -351,6 +372,7 @@ def main():
     ism_cases()
     decay_cases()
     container_case()
+    generate_case()
     for f in sorted(OUT.iterdir()):
         print(f.name, f.stat().st_size)
 
