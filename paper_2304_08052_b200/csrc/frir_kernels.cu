@@ -410,7 +410,7 @@ struct TailArgs {
   int total_channels;
 };
 
-constexpr int kTailThreads = 256;
+constexpr int kTailThreads = 128;
 constexpr int kTailWarps = kTailThreads / 32;
 
 __global__ void __launch_bounds__(kTailThreads) tail_kernel(const __grid_constant__ TailArgs A) {

@@ -156,8 +156,22 @@ class MixtureResult:
 
 
 def fft_size(n: int) -> int:
-    """Power-of-two FFT length holding a linear convolution of length n."""
-    return 1 << max(0, int(n - 1).bit_length())
+    """Smallest 2^a 3^b 5^c (an efficient cuFFT length) holding a linear
+    convolution of length n: at most ~1.25 n instead of up to 2 n for a power
+    of two."""
+    n = max(1, int(n))
+    best = 1 << max(0, (n - 1).bit_length())
+    p5 = 1
+    while p5 < best:
+        p35 = p5
+        while p35 < best:
+            m = p35
+            while m < n:
+                m *= 2
+            best = min(best, m)
+            p35 *= 3
+        p5 *= 5
+    return best
 
 
 def _torch():

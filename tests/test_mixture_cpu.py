@@ -27,8 +27,16 @@ def test_spec_validation(kw, msg):
 
 
 def test_fft_size():
-    assert MX.fft_size(1) == 1 and MX.fft_size(2) == 2 and MX.fft_size(3) == 4
-    assert MX.fft_size(70399) == 131072 and MX.fft_size(65536) == 65536
+    assert MX.fft_size(1) == 1 and MX.fft_size(2) == 2 and MX.fft_size(3) == 3 and MX.fft_size(7) == 8
+    assert MX.fft_size(65536) == 65536 and MX.fft_size(70399) == 72000
+    for n in (1, 17, 1000, 70399, 131073, 999999):
+        m = MX.fft_size(n)
+        assert m >= n and m < 1.25 * n + 8
+        r = m
+        for p in (2, 3, 5):
+            while r % p == 0:
+                r //= p
+        assert r == 1
 
 
 @pytest.mark.parametrize("ci", [4, 5])
