@@ -586,6 +586,10 @@ struct RenderArgs {
   float* out_early;
 };
 
+__device__ __forceinline__ void sts_f32(unsigned addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+constexpr int kTileRow = kTile + 2 * kWin;  // tile buffer row: 2 scratch windows + the tile
 constexpr int kRenderThreads = 384;  // 12 warps: the shared tables amortise over more warps
 constexpr int kWarps = kRenderThreads / 32;
 __device__ __forceinline__ int ceil_div_i(int a, int b) {  // b > 0, any sign of a
@@ -742,8 +746,10 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(const __grid_
   const int ncomp = d.r_h * kRow;
   float2* s_comp = reinterpret_cast<float2*>(smem);
   double* s_corr_all = reinterpret_cast<double*>(smem + (size_t)ncomp * 8);  // [warp][V][32]
-  float* s_tile = reinterpret_cast<float*>(s_corr_all + kWarps * V * 32);  // [warp][V][D, W][kTile]
-  int2* s_items = reinterpret_cast<int2*>(s_tile + (size_t)kWarps * V * 2 * kTile);
+  // [warp][V][D, W][2 scratch windows + kTile]: emits of windows -2, -1 land
+  // in the scratch windows, so the per-window store needs no branch
+  float* s_tile = reinterpret_cast<float*>(s_corr_all + kWarps * V * 32);
+  int2* s_items = reinterpret_cast<int2*>(s_tile + (size_t)kWarps * V * 2 * kTileRow);
   float* s_head = reinterpret_cast<float*>(s_items + 32 * kWarps);          // [warp][V][D, W][64]
   for (int i = threadIdx.x; i < ncomp; i += blockDim.x) s_comp[i] = A.plan.comp[i];
   __syncthreads();
@@ -751,10 +757,11 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(const __grid_
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned comp_sh = (unsigned)__cvta_generic_to_shared(s_comp);
   const unsigned lane8 = 8u * lane;
-  float* dF_t = s_tile + (size_t)warp * V * 2 * kTile;
-  float* wF_t = dF_t + kTile;
-  float* dE_t = wF_t + kTile;
-  float* wE_t = dE_t + kTile;
+  float* dF_t = s_tile + (size_t)warp * V * 2 * kTileRow + 2 * kWin;  // window 0 of the tile
+  float* wF_t = dF_t + kTileRow;
+  float* dE_t = wF_t + kTileRow;
+  float* wE_t = dE_t + kTileRow;
+  const unsigned t_sh = (unsigned)__cvta_generic_to_shared(dF_t) + 4u * lane;  // emit stores: slot * 128 B
   double* corrF_s = s_corr_all + warp * V * 32;
   double* corrE_s = corrF_s + 32;
   int2* s_it = s_items + 32 * warp;
@@ -852,7 +859,8 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(const __grid_
     bool e_dead = false;  // early ring-down negligible: outputs are zeros
     double e_ref = 0.0;   // largest early LP state seen while early items fed tiles
     int w = -2;           // window held by the front accumulators
-    int slot = 0;         // next tile slot
+    int slot = -2;        // next tile slot (negative: scratch windows)
+    bool est = true;      // the current tile is not quiet: early windows are stored
     auto flush = [&]() {
       const int w0 = w - slot + 1;  // first window of the tile
       const int n_base = w0 * kWin - kExt;
@@ -860,6 +868,17 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(const __grid_
         wF_t[s2 * kWin + lane] = 0.f;
         dF_t[s2 * kWin + lane] = 0.f;
         if (EARLY) { wE_t[s2 * kWin + lane] = 0.f; dE_t[s2 * kWin + lane] = 0.f; }
+      }
+      if (head_on && w0 == 0) {  // head corrections of windows 0 and 1 (warp-uniform, once)
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2) {
+          dF_t[s2 * kWin + lane] += head_s[32 * s2 + lane];
+          wF_t[s2 * kWin + lane] += head_s[64 + 32 * s2 + lane];
+          if (EARLY) {
+            dE_t[s2 * kWin + lane] += head_s[128 + 32 * s2 + lane];
+            wE_t[s2 * kWin + lane] += head_s[192 + 32 * s2 + lane];
+          }
+        }
       }
       __syncwarp();
       double lp[kChunk];
@@ -894,26 +913,18 @@ __global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(const __grid_
       }
       __syncwarp();
       slot = 0;
+      est = w + 1 <= ew_hi;  // the next tile starts at window w + 1
     };
     auto emit = [&]() {
-      if (w >= 0) {
-        if (head_on && w < 2) {  // warp-uniform, at most twice per channel
-          ch.dF[0] += head_s[32 * w + lane];
-          ch.wF[0] += head_s[64 + 32 * w + lane];
-          if (EARLY) {
-            ch.dE[0] += head_s[128 + 32 * w + lane];
-            ch.wE[0] += head_s[192 + 32 * w + lane];
-          }
-        }
-        dF_t[slot * kWin + lane] = ch.dF[0];
-        wF_t[slot * kWin + lane] = ch.wF[0];
-        if (EARLY && w - slot <= ew_hi) {  // tile not quiet: its early slots are read
-          dE_t[slot * kWin + lane] = ch.dE[0];
-          wE_t[slot * kWin + lane] = ch.wE[0];
-        }
-        ++slot;
-        if (slot == kTileWin || w == nwin - 1) flush();
+      const unsigned a = t_sh + (unsigned)(slot * (kWin * 4));
+      sts_f32(a, ch.dF[0]);
+      sts_f32(a + kTileRow * 4, ch.wF[0]);
+      if (EARLY && est) {  // tile not quiet: its early slots are read
+        sts_f32(a + 2 * kTileRow * 4, ch.dE[0]);
+        sts_f32(a + 3 * kTileRow * 4, ch.wE[0]);
       }
+      ++slot;
+      if (slot == kTileWin || w == nwin - 1) flush();
       ch.shift();
       ++w;
     };
@@ -974,7 +985,7 @@ static int table_blocks(const frir_plan_desc& d) { return (d.sup + 31) / 32; }
 static size_t render_smem(const frir_plan_desc& d, bool early) {
   const int v = early ? 2 : 1;
   return (size_t)d.r_h * 64 * table_blocks(d) * 8 + (size_t)kWarps * v * 32 * 8 +
-         (size_t)kWarps * v * 2 * kTile * 4 + (size_t)kWarps * 32 * 8 +
+         (size_t)kWarps * v * 2 * kTileRow * 4 + (size_t)kWarps * 32 * 8 +
          (size_t)kWarps * v * 2 * 64 * 4;
 }
 
