@@ -325,3 +325,52 @@ def test_random_scenes_match_oracle(seed):
         assert rel_err(full[m], full_o[m]) <= TOL, (seed, job.sample_rate, m)
         assert rel_err(early[m], early_o[m]) <= TOL, (seed, job.sample_rate, m)
     assert np.array_equal(res.direct_index.cpu().numpy(), direct_o)
+
+
+def test_ragged_batch_one_launch():
+    """One launch over jobs with different image counts (incl. 0), mic counts
+    (1 and 12), T60s (30 ms .. 1.2 s) and sources: each equals the oracle."""
+    rng = np.random.default_rng(77)
+    specs = [(0, 1, 0.3), (5, 12, 0.05), (2048, 3, 1.2), (300, 1, 0.03), (4096, 12, 0.6), (1, 2, 0.2)]
+    jobs = engine.new_jobs(len(specs))
+    mic_rows, ojobs, off = [], [], 0
+    for j, (n, m, t60) in enumerate(specs):
+        mics = rng.uniform(-0.1, 0.1, size=(m, 3))
+        src = (float(rng.uniform(0.5, 2.0)), float(rng.uniform(0, 6.28)), float(rng.uniform(-0.4, 0.4)))
+        room = (5.0, 4.5, 3.0)
+        jobs[j]["room"], jobs[j]["center"] = room, mics.mean(axis=0)
+        jobs[j]["d0"], jobs[j]["az"], jobs[j]["el"] = src
+        jobs[j]["t60"], jobs[j]["seed"], jobs[j]["n_images"] = t60, 100 + j, n
+        jobs[j]["mic_off"], jobs[j]["n_mics"] = off, m
+        off += m
+        mic_rows.append(mics)
+        ojobs.append(P.Job(room=room, mics=mics, center=mics.mean(axis=0), source=src, t60=t60,
+                           num_images=n, seed=100 + j))
+    res = engine.simulate_jobs(16000, jobs, np.concatenate(mic_rows))
+    d = res.direct_index.cpu().numpy()
+    for j, job in enumerate(ojobs):
+        full_o, early_o, direct_o = P.render(job)
+        full = res.job_view(j).cpu().numpy()
+        early = res.job_view(j, "early").cpu().numpy()
+        for m in range(len(job.mics)):
+            assert rel_err(full[m], full_o[m]) <= TOL, (j, m)
+            assert rel_err(early[m], early_o[m]) <= TOL, (j, m)
+        ch = int(res.prepared.jobs[j]["chan_off"])
+        assert np.array_equal(d[ch: ch + len(job.mics)], direct_o)
+
+
+def test_wide_sort_path_large_image_list():
+    """> 65535 images per job: the sort switches to 32-bit counters."""
+    mics = np.array([[0.0, 0.0, 0.0], [0.06, 0.0, 0.0]])
+    jobs = engine.new_jobs(1)
+    jobs["room"] = (7.0, 6.0, 3.0)
+    jobs["center"] = mics.mean(axis=0)
+    jobs["d0"], jobs["az"], jobs["el"] = 1.7, 0.4, 0.0
+    jobs["t60"], jobs["seed"], jobs["n_images"], jobs["n_mics"] = 0.4, 9, 70000, 2
+    res = engine.simulate_jobs(16000, jobs, mics)
+    job = P.Job(room=(7.0, 6.0, 3.0), mics=mics, center=mics.mean(axis=0), source=(1.7, 0.4, 0.0), t60=0.4,
+                num_images=70000, seed=9)
+    full_o, early_o, _ = P.render(job)
+    for m in range(2):
+        assert rel_err(res.job_view(0).cpu().numpy()[m], full_o[m]) <= TOL
+        assert rel_err(res.job_view(0, "early").cpu().numpy()[m], early_o[m]) <= TOL
