@@ -52,6 +52,12 @@ def _cpu_item(args):
     from oracle import mixture_port as MP
 
     spec_dict, scene, prm, dry, noise, offsets, sir, snr = args
+    from paper_2304_08052_b200 import mixture as MX  # the same host material generator
+
+    pool = MX.SyntheticPool()
+    rng = np.random.default_rng(0)
+    for _ in range(len(dry) + 1):
+        pool.draw(rng, len(noise), 16000)
     rirs_f, rirs_e = [], []
     for job in P.jobs_from_scene(prm, scene):
         full, early, _ = P.render(job)
@@ -128,6 +134,22 @@ def main():
         "config": {"workload": f"{B} utterances: 2 speakers + noise, 4 mics, 4 s @ 16 kHz, 2048 images, "
                                "full+early RIRs, FFT convolution (cuFFT) + frir_mix_* kernels"},
     }
+    # e2e: the public drop-in generate_batch -- host draws in the reference's
+    # order on all host cores (threads), RIRs + mix on the device, results
+    # copied back to host numpy arrays -- wall clock per batch
+    cores = len(os.sched_getaffinity(0))
+    MX.generate_batch(min(B, 8), spec, seed=1, workers=cores)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = MX.generate_batch(B, spec, seed=2, workers=cores)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    d2h = sum(r.mixture.nbytes + sum(x.nbytes for x in r.sources) + sum(x.nbytes for x in r.early_sources)
+              + r.noise.nbytes for r in res)
+    h2d = B * (S + 1) * N * 4
+    line["e2e"] = {"value": B / wall, "unit": "mixtures/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                   "path": f"mixture.generate_batch({B}, MixtureSpec(), workers={cores}): host draws (threads) "
+                           "+ device RIRs + device mix + D2H of all outputs"}
     if not a.no_cpu_baseline:
         n = min(a.cpu_items, B)
         cores = len(os.sched_getaffinity(0))
@@ -138,8 +160,8 @@ def main():
             list(ex.map(_cpu_item, args))
         wall = time.perf_counter() - t0
         line["cpu_baseline"] = {"value": n / wall, "unit": "mixtures/s", "cores": min(cores, n), "kind": "port",
-                                "sample": f"first {n} utterances: oracle/framrir_port RIRs + oracle/mixture_port "
-                                          f"mixing (numpy/scipy FP64), wall {wall:.2f} s"}
+                                "sample": f"first {n} utterances: SyntheticPool draws + oracle/framrir_port RIRs + "
+                                          f"oracle/mixture_port mixing (numpy/scipy FP64), wall {wall:.2f} s"}
     print(json.dumps(line))
 
 

@@ -387,6 +387,29 @@ def spatialize_and_mix(sources: list, noise: np.ndarray, rirs: list, spec: Mixtu
     )
 
 
+def _item_draws(args):
+    """Host draws of one utterance in the reference's order (mixture.py:335-342,
+    then spatialize_and_mix's offsets / SIR / SNR, :245-263)."""
+    spec, curriculum, seed, i, pool = args
+    S = spec.n_speakers
+    fs = spec.sample_rate
+    n_dry = int(spec.utterance_seconds * spec.sample_rate)
+    rng = np.random.Generator(np.random.Philox(np.random.SeedSequence((int(seed), int(i)))))
+    sc, pr = sample_scene(spec, rng, curriculum)
+    srcs = [pool.draw(rng, n_dry, fs) for _ in range(S)]
+    nz = pool.draw(rng, n_dry, fs)
+    offs = _draw_offsets(srcs, spec, rng)
+    for k in range(1, S):
+        achieved = _overlap_ratio(len(srcs[0]), offs[k], len(srcs[k]))
+        if achieved < spec.min_overlap_ratio:
+            raise ValueError(f"speaker {k} overlap ratio {achieved:.2f} is below the "
+                             f"required {spec.min_overlap_ratio}")
+    sir = [float(rng.uniform(*spec.sir_db)) for _ in range(S - 1)]
+    snr = float(rng.uniform(*spec.snr_db))
+    return (sc, pr, np.stack([np.asarray(x, dtype=np.float32) for x in srcs]), np.asarray(nz, dtype=np.float32),
+            offs, sir, snr)
+
+
 def generate_batch(batch_size: int, spec: MixtureSpec, curriculum: CurriculumState | None = None, seed: int = 0,
                    workers: int = 1, pool=None, executor=None, *, device=None) -> list:
     """``batch_size`` independent utterances (drop-in for mixture.py:365-395).
@@ -396,8 +419,8 @@ def generate_batch(batch_size: int, spec: MixtureSpec, curriculum: CurriculumSta
     and noise, offsets, SIR, SNR -- so the content matches the reference item
     for item.  All RIRs of the batch then render in ONE device launch (full +
     early, (n_speakers + 1) sources per item) and are mixed on the device in
-    one ``mix_device`` call.  ``workers`` / ``executor`` are accepted for
-    signature compatibility; the device does the parallel work.
+    one ``mix_device`` call.  ``workers`` (threads) or ``executor`` (any
+    ``map``-capable executor) parallelise the host draws.
     """
     if batch_size < 0:
         raise ValueError("batch_size must be >= 0")
@@ -410,25 +433,20 @@ def generate_batch(batch_size: int, spec: MixtureSpec, curriculum: CurriculumSta
     S = spec.n_speakers
     fs = spec.sample_rate
     n_dry = int(spec.utterance_seconds * spec.sample_rate)
-    scenes, params, dry, noises, offsets, sirs, snrs = [], [], [], [], [], [], []
-    for i in range(batch_size):  # mixture.py:335-342, then spatialize_and_mix's draws (:245-263)
-        rng = np.random.Generator(np.random.Philox(np.random.SeedSequence((int(seed), int(i)))))
-        sc, pr = sample_scene(spec, rng, curriculum)
-        srcs = [pool.draw(rng, n_dry, fs) for _ in range(S)]
-        nz = pool.draw(rng, n_dry, fs)
-        offs = _draw_offsets(srcs, spec, rng)
-        for k in range(1, S):
-            achieved = _overlap_ratio(len(srcs[0]), offs[k], len(srcs[k]))
-            if achieved < spec.min_overlap_ratio:
-                raise ValueError(f"speaker {k} overlap ratio {achieved:.2f} is below the "
-                                 f"required {spec.min_overlap_ratio}")
-        sirs.append([float(rng.uniform(*spec.sir_db)) for _ in range(S - 1)])
-        snrs.append(float(rng.uniform(*spec.snr_db)))
-        scenes.append(sc)
-        params.append(pr)
-        dry.append(np.stack([np.asarray(x, dtype=np.float32) for x in srcs]))
-        noises.append(np.asarray(nz, dtype=np.float32))
-        offsets.append(offs)
+    # per-item streams are independent: the host draws run on `executor`
+    # (e.g. a warm ProcessPoolExecutor, as the reference takes one) or on
+    # `workers` threads (numpy/scipy release the GIL in the bulk work)
+    args = [(spec, curriculum, seed, i, pool) for i in range(batch_size)]
+    if executor is not None:
+        items = list(executor.map(_item_draws, args))
+    elif workers > 1 and batch_size > 1:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(max_workers=workers) as ex:
+            items = list(ex.map(_item_draws, args))
+    else:
+        items = [_item_draws(a) for a in args]
+    scenes, params, dry, noises, offsets, sirs, snrs = (list(x) for x in zip(*items))
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     jobs, mics = scene_batch_jobs(scenes, params)
     pb = engine.prepare(fs, jobs, mics, padded=True)
@@ -437,15 +455,20 @@ def generate_batch(batch_size: int, spec: MixtureSpec, curriculum: CurriculumSta
     M = len(scenes[0].mic_positions)
     stride = int(pb.jobs[0]["out_stride"])
     rir_len = pb.jobs["n2"].reshape(B, S + 1)[:, 0]
-    out = mix_device(torch.as_tensor(np.stack(dry), device=dev), [[n_dry] * S] * B, offsets,
-                     torch.as_tensor(np.stack(noises), device=dev), [n_dry] * B,
+    dry_p = torch.from_numpy(np.stack(dry)).pin_memory()
+    noise_p = torch.from_numpy(np.stack(noises)).pin_memory()
+    out = mix_device(dry_p.to(dev, non_blocking=True), [[n_dry] * S] * B, offsets,
+                     noise_p.to(dev, non_blocking=True), [n_dry] * B,
                      res.full.view(B, S + 1, M, stride), res.early.view(B, S + 1, M, stride), rir_len,
                      [x if S > 1 else [0.0] for x in sirs], snrs, sir_scope=spec.sir_scope)
-    mix_h = out["mixture"].cpu().numpy()
-    src_h = out["sources"].cpu().numpy()
-    early_h = out["early"].cpu().numpy()
-    noise_h = out["noise"].cpu().numpy()
-    gains = out["gains"].cpu().numpy()
+    # device -> pinned host (the per-item arrays below are views into these;
+    # each view keeps its pinned block alive)
+    host = {k: torch.empty(out[k].shape, dtype=out[k].dtype, pin_memory=True)
+            for k in ("mixture", "sources", "early", "noise")}
+    for k, t in host.items():
+        t.copy_(out[k], non_blocking=True)
+    gains = out["gains"].cpu().numpy()  # synchronises the stream
+    mix_h, src_h, early_h, noise_h = (host[k].numpy() for k in ("mixture", "sources", "early", "noise"))
     results = []
     for b in range(B):
         T = int(out["total"][b])
@@ -465,10 +488,10 @@ def generate_batch(batch_size: int, spec: MixtureSpec, curriculum: CurriculumSta
             "distances": [float(x[0]) for x in np.atleast_2d(scenes[b].sources)],
         }
         results.append(MixtureResult(
-            mixture=mix_h[b, :, :T].copy(),
-            sources=[src_h[b, k, :, :T].copy() for k in range(S)],
-            early_sources=[early_h[b, k, :, :T].copy() for k in range(S)],
-            noise=noise_h[b, :, :T].copy(),
+            mixture=mix_h[b, :, :T],
+            sources=[src_h[b, k, :, :T] for k in range(S)],
+            early_sources=[early_h[b, k, :, :T] for k in range(S)],
+            noise=noise_h[b, :, :T],
             metadata=md,
         ))
     return results
