@@ -134,6 +134,25 @@ def main():
         "config": {"workload": f"{B} utterances: 2 speakers + noise, 4 mics, 4 s @ 16 kHz, 2048 images, "
                                "full+early RIRs, FFT convolution (cuFFT) + frir_mix_* kernels"},
     }
+    # device scene sampler: rooms drawn on the GPU straight
+    # into render jobs, then all their RIRs in one launch
+    from paper_2304_08052_b200.sampler import DeviceSceneSampler
+
+    smp = DeviceSceneSampler(spec)
+    nroom = 1024
+    smp.render(seed=11, first=0, count=nroom)
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for r in range(3):
+        smp.render(seed=12 + r, first=0, count=nroom)
+    s1.record()
+    torch.cuda.synchronize()
+    ms_s = s0.elapsed_time(s1) / 3
+    line["device_sampler"] = {"value": nroom * (S + 1) / ms_s * 1e3, "unit": "RIR/s",
+                              "ms_per_batch": ms_s,
+                              "workload": f"{nroom} sample_scene draws on the device -> {nroom * (S + 1)} "
+                                          f"{M}-channel full+early RIRs (2048 images), one launch"}
     # e2e: the public drop-in generate_batch -- host draws in the reference's
     # order on all host cores (threads), RIRs + mix on the device, results
     # copied back to host numpy arrays -- wall clock per batch

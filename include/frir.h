@@ -245,6 +245,34 @@ int frir_mix_combine(const float* y, const double* gains, const int32_t* total, 
                      int32_t M, int64_t F, int64_t T, float* mixture, float* sources, float* early,
                      float* noise, void* stream);
 
+/* ---- on-device scene sampler (mixture.py:171-213) ----
+   Items first_index .. first_index + count - 1 of sample_scene's stream
+   Philox(SeedSequence((seed, index))): room, T60, then n_sources placements
+   (distance, azimuth, elevation) and the simulation seed, bit-identical to
+   numpy's draws; written as n_sources render jobs per item (SimParams
+   defaults for the other knobs, the reference's validation rules) with a
+   fixed row stride, plus chan_job, and a per-item status (0 ok; 1 aperture
+   not below the smallest room dimension; 2 c0*t60 not above a source
+   distance; 3 reflection / rr_max rule; 4 T60 longer than out_stride allows).
+   Jobs are ready for frir_simulate with batch totals computed by the caller
+   from the fixed sizes. */
+typedef struct {
+  double room_length[2], room_width[2], room_height[2];  /* uniform ranges */
+  double t60[2];             /* spec.t60_range or the curriculum bounds */
+  double distance[2];        /* spec.speaker_distance */
+  double elevation[2];       /* spec.elevation_range */
+  double center[3];          /* array reference point (mic centroid) */
+  double aperture;           /* largest mic-to-mic distance */
+  double c0;                 /* sound speed */
+  double alpha3, b3a3;       /* alpha**3, beta**3 - alpha**3 of the SimParams defaults (host pow) */
+  int32_t n_sources;         /* speakers + point noise */
+  int32_t n_mics;
+  int32_t num_images;
+  int32_t out_stride;        /* floats per channel row: >= max n2, multiple of 4 */
+} frir_scene_spec;
+int frir_sample_scene_jobs(const frir_plan* plan, const frir_scene_spec* spec, uint64_t seed, int64_t first_index,
+                           int32_t count, frir_job* jobs, int32_t* chan_job, int32_t* status, void* stream);
+
 /* ---- batched decay measurement (decay.py:8-49) ----
    Rows h[c][0:len[c]] (float32, row stride ld floats).  frir_edc writes the
    unnormalised energy decay curve edc[c][i] = sum_{j>=i} h[c][j]^2 in FP64,

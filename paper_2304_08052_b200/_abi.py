@@ -68,6 +68,16 @@ class FrirBatch(ctypes.Structure):
     ]
 
 
+class FrirSceneSpec(ctypes.Structure):
+    _fields_ = [
+        ("room_length", c_double * 2), ("room_width", c_double * 2), ("room_height", c_double * 2),
+        ("t60", c_double * 2), ("distance", c_double * 2), ("elevation", c_double * 2),
+        ("center", c_double * 3), ("aperture", c_double), ("c0", c_double), ("alpha3", c_double),
+        ("b3a3", c_double), ("n_sources", c_int32), ("n_mics", c_int32), ("num_images", c_int32),
+        ("out_stride", c_int32),
+    ]
+
+
 JOB_DTYPE = np.dtype(FrirJob)
 
 # (name, restype, argtypes) of every symbol include/frir.h declares.
@@ -105,6 +115,9 @@ SIGNATURES = [
     ("frir_mix_combine", c_int32,
      [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int64, c_int64, c_void_p, c_void_p,
       c_void_p, c_void_p, c_void_p]),
+    ("frir_sample_scene_jobs", c_int32,
+     [c_void_p, ctypes.POINTER(FrirSceneSpec), c_uint64, c_int64, c_int32, c_void_p, c_void_p, c_void_p,
+      c_void_p]),
     ("frir_edc", c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_int64, c_void_p, c_void_p]),
     ("frir_t60", c_int32,
      [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_int64, c_void_p, c_double, c_double, c_double,

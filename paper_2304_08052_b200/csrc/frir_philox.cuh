@@ -77,11 +77,12 @@ struct SeedMixer {
 };
 
 // SeedSequence((seed, k, stage)).generate_state(2, np.uint64)
-FRIR_HD void seed_keys(uint64_t seed, uint64_t k, uint64_t stage, uint64_t key[2]) {
+// Keys of Philox(SeedSequence(tuple(vals[0:nv]))) for nv <= 3 non-negative
+// 64-bit integers (numpy's entropy: each int as little-endian uint32 words).
+FRIR_HD void seed_keys_n(const uint64_t* vals, int nv, uint64_t key[2]) {
   uint32_t ent[6];
   int n = 0;
-  uint64_t vals[3] = {seed, k, stage};
-  for (int v = 0; v < 3; ++v) {
+  for (int v = 0; v < nv; ++v) {
     uint64_t x = vals[v];
     if (x == 0) {
       ent[n++] = 0;
@@ -112,6 +113,11 @@ FRIR_HD void seed_keys(uint64_t seed, uint64_t k, uint64_t stage, uint64_t key[2
   }
   key[0] = (uint64_t)st[0] | ((uint64_t)st[1] << 32);
   key[1] = (uint64_t)st[2] | ((uint64_t)st[3] << 32);
+}
+
+FRIR_HD void seed_keys(uint64_t seed, uint64_t k, uint64_t stage, uint64_t key[2]) {
+  const uint64_t vals[3] = {seed, k, stage};
+  seed_keys_n(vals, 3, key);
 }
 
 // Word `w` of the stream keyed by `key`: block w/4 (counter w/4 + 1), lane w%4.
