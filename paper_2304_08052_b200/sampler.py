@@ -116,8 +116,10 @@ class DeviceSceneSampler:
         b.max_rows = rows
         b.max_windows = self.max_windows
         lib = _abi.lib()
-        ws = torch.empty(int(lib.frir_workspace_size(self.plan.handle, ctypes.byref(b))), dtype=torch.uint8,
-                         device=self.device)
+        need = int(lib.frir_workspace_size(self.plan.handle, ctypes.byref(b)))
+        ws = getattr(self, "_ws", None)
+        if ws is None or ws.numel() < need:  # the workspace is reused across calls
+            ws = self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
         full = torch.zeros(int(b.total_out), dtype=torch.float32, device=self.device)
         early = torch.zeros_like(full) if include_early else None
         direct = torch.empty(int(b.total_channels), dtype=torch.int32, device=self.device)
