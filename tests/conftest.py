@@ -49,3 +49,17 @@ def _built_library():
     from paper_2304_08052_b200 import build
 
     build.build()
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _debug_bounds_checks():
+    """With FRIR_LIB pointing at libfrir_debug.so (build.py --debug), every
+    kernel index is bounds-checked; fail the session if any check fired."""
+    yield
+    import os
+
+    if "debug" in os.environ.get("FRIR_LIB", ""):
+        from paper_2304_08052_b200 import _abi
+
+        line = _abi.lib().frir_debug_status()
+        assert line == 0, f"a device bounds check failed at frir_kernels.cu:{line}"
