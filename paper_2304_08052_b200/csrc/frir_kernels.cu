@@ -292,8 +292,6 @@ struct SortArgs {
   int r_h, t0;
 };
 
-constexpr int kSortThreads = 256;
-constexpr int kSortWarps = kSortThreads / 32;
 
 // Two passes over the channel's raw items (K1's output, read twice; the second
 // read hits L2): per-warp 16-bit bucket histograms over contiguous row chunks,
@@ -309,8 +307,9 @@ __device__ __forceinline__ void count_add(CT* cnt, int idx) {
     atomicAdd(reinterpret_cast<unsigned*>(cnt) + idx, 1u);
 }
 
-template <typename CT>
-__global__ void __launch_bounds__(kSortThreads) sort_kernel(SortArgs A) {
+template <typename CT, int NW>  // NW warps per channel (more for long rows)
+__global__ void __launch_bounds__(NW * 32) sort_kernel(SortArgs A) {
+  constexpr int kSortWarps = NW, kSortThreads = NW * 32;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_wsum[kSortWarps];
   const int c = blockIdx.x;
@@ -1052,11 +1051,14 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_
     sa.r_h = d.r_h; sa.t0 = d.t0; sa.plan = plan->dev;
     const int nbk = ((b->max_windows * kWin + kSpBias) >> 5) + 3;
     const bool wide = b->max_rows > 65535;  // sorted positions need 32-bit counters
-    const size_t smem = align16((size_t)nbk * kSortWarps * (wide ? 4 : 2));
-    auto kern = wide ? sort_kernel<uint32_t> : sort_kernel<uint16_t>;
+    const bool big = b->total_items >= 4096LL * b->total_channels;  // long rows on average: 16 warps
+    const int nw = big ? 16 : 8;
+    const size_t smem = align16((size_t)nbk * nw * (wide ? 4 : 2));
+    auto kern = wide ? (big ? sort_kernel<uint32_t, 16> : sort_kernel<uint32_t, 8>)
+                     : (big ? sort_kernel<uint16_t, 16> : sort_kernel<uint16_t, 8>);
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess) {
-      kern<<<b->total_channels, kSortThreads, smem, st>>>(sa);
+      kern<<<b->total_channels, nw * 32, smem, st>>>(sa);
       e = cudaGetLastError();
     }
     if (e != cudaSuccess) { set_error(std::string("sort_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
