@@ -589,7 +589,7 @@ __device__ __forceinline__ void sts_f32(unsigned addr, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
 constexpr int kTileRow = kTile + 2 * kWin;  // tile buffer row: 2 scratch windows + the tile
-constexpr int kRenderThreads = 384;  // 12 warps: the shared tables amortise over more warps
+constexpr int kRenderThreads = 256;  // 8 warps x 3 CTAs per SM
 constexpr int kWarps = kRenderThreads / 32;
 __device__ __forceinline__ int ceil_div_i(int a, int b) {  // b > 0, any sign of a
   return a >= 0 ? (a + b - 1) / b : -((-a) / b);
@@ -737,7 +737,7 @@ struct Channel {
 };
 
 template <bool EARLY, int NBK>
-__global__ void __launch_bounds__(kRenderThreads, 2) render_kernel(const __grid_constant__ RenderArgs A) {
+__global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(const __grid_constant__ RenderArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const frir_plan_desc& d = A.plan.d;
   constexpr int kRow = 64 * NBK;  // doubled rows (see Channel::add)
