@@ -176,3 +176,37 @@ def test_jobs_prepare_ism_rules():
     j["kind"] = 7
     with pytest.raises(ValueError, match="unknown job kind"):
         engine.prepare(16000, j, MICS)
+
+
+def test_header_compiles_as_c_and_links(tmp_path):
+    """include/frir.h is plain C (C99): a C program includes it, links
+    libfrir.so and calls the host-only entry points."""
+    import shutil
+    import subprocess
+
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc not available")
+    src = tmp_path / "abi.c"
+    src.write_text(r"""
+#include <stdio.h>
+#include "frir.h"
+int main(void) {
+  frir_plan_desc d;
+  if (frir_abi_version() != FRIR_ABI_VERSION) return 2;
+  if (frir_design_describe(16000, &d) != FRIR_OK) return 3;
+  if (d.r_h != 62 || d.r_l != 7) return 4;
+  if (frir_struct_size(0) != (int64_t)sizeof(frir_job)) return 5;
+  if (frir_struct_size(1) != (int64_t)sizeof(frir_batch)) return 6;
+  if (frir_design_describe(1000000, &d) == FRIR_OK) return 7;   /* rejected like rate_factors */
+  printf("%s\n", frir_last_error());
+  return 0;
+}
+""")
+    lib = Path(_abi.LIB_PATH)
+    exe = tmp_path / "abi"
+    subprocess.run([gcc, "-std=c99", "-Wall", "-Werror", "-I", str(HEADER.parent), str(src), "-o", str(exe),
+                    "-L", str(lib.parent), "-lfrir", f"-Wl,-rpath,{lib.parent}"], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0, out
+    assert out.stdout.strip()  # the rejection left a message
