@@ -138,7 +138,7 @@ class BatchResult:
 class DeviceBatch:
     """Device-resident copy of a prepared batch plus its workspace."""
 
-    def __init__(self, pb: PreparedBatch, device=None, stream=None):
+    def __init__(self, pb: PreparedBatch, device=None, stream=None, workspace: bool = True):
         require_cuda()
         self.pb = pb
         dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index)
@@ -161,8 +161,10 @@ class DeviceBatch:
         if self.draws is not None:
             b.draw_dist, b.draw_az, b.draw_el, b.draw_refl = (d.data_ptr() for d in self.draws)
         self.batch = b
-        ws = _abi.lib().frir_workspace_size(self.plan.handle, ctypes.byref(b))
-        self.workspace = torch.empty(int(ws), dtype=torch.uint8, device=dev)
+        self.workspace_bytes = int(_abi.lib().frir_workspace_size(self.plan.handle, ctypes.byref(b)))
+        # workspace=False: the caller passes one to launch() (shared / double-buffered)
+        self.workspace = (torch.empty(self.workspace_bytes, dtype=torch.uint8, device=dev) if workspace
+                          else None)
 
     def alloc_outputs(self, include_early: bool = True):
         n = int(self.batch.total_out)
@@ -175,12 +177,16 @@ class DeviceBatch:
         direct = torch.empty(int(self.batch.total_channels), dtype=torch.int32, device=self.device)
         return full, early, direct
 
-    def launch(self, full, early, direct, stream=None, stages: int = _abi.STAGE_ALL) -> None:
-        """Enqueue the render of the whole batch on `stream` (default: current)."""
+    def launch(self, full, early, direct, stream=None, stages: int = _abi.STAGE_ALL, workspace=None) -> None:
+        """Enqueue the render of the whole batch on `stream` (default: current),
+        using `workspace` (uint8 device tensor >= workspace_bytes) if given."""
         st = torch.cuda.current_stream(self.device) if stream is None else stream
+        ws = self.workspace if workspace is None else workspace
+        if ws is None or ws.numel() < self.workspace_bytes:
+            raise ValueError(f"workspace too small: need {self.workspace_bytes} bytes")
         status = _abi.lib().frir_simulate_stages(
-            self.plan.handle, ctypes.byref(self.batch), self.workspace.data_ptr(),
-            self.workspace.numel(), full.data_ptr(), early.data_ptr() if early is not None else None,
+            self.plan.handle, ctypes.byref(self.batch), ws.data_ptr(),
+            ws.numel(), full.data_ptr(), early.data_ptr() if early is not None else None,
             direct.data_ptr(), st.cuda_stream, stages,
         )
         _abi.check(status, "frir_simulate_stages")
