@@ -12,8 +12,6 @@
 //                     correction, coalesced full + early stores
 //                                                             resample.py:81-136
 // No atomics touch sample values, so outputs are bit-reproducible.
-#include <cstdlib>
-
 #include "frir_internal.h"
 #include "frir_philox.cuh"
 
@@ -1001,7 +999,6 @@ static cudaError_t launch_render(const RenderArgs& ra, const frir_plan_desc& d, 
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, render_kernel<EARLY, NBK>, kRenderThreads, smem);
-  if (const char* cap = getenv("FRIR_RENDER_CTAS_PER_SM")) per_sm = std::min(per_sm, atoi(cap));  // experiment knob
   if (per_sm < 1) per_sm = 1;
   long want = (channels + kWarps - 1) / kWarps;
   int grid = (int)std::min<long>((long)sms * per_sm, want);
