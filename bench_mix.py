@@ -132,7 +132,7 @@ def main():
         "ms_per_step": ms, "mix_only_ms": mix_ms, "higher_is_better": True, "dtype": "f32 (FP64 powers/gains)",
         "data": "synthetic: MixtureSpec() scenes (sample_scene draws), seeded Gaussian dry signals",
         "config": {"workload": f"{B} utterances: 2 speakers + noise, 4 mics, 4 s @ 16 kHz, 2048 images, "
-                               "full+early RIRs, FFT convolution (cuFFT) + frir_mix_* kernels"},
+                               "full+early RIRs, frir_mix_convolve (own 8192-point partitioned FFT convolution) + frir_mix_* kernels"},
     }
     # device scene sampler: rooms drawn on the GPU straight
     # into render jobs, then all their RIRs in one launch

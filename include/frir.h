@@ -227,6 +227,19 @@ int frir_mix_pack_dry(const float* dry, int64_t dry_stride_b, int64_t dry_stride
 int frir_mix_pack_filters(const float* rir_full, int64_t full_stride_b, const float* rir_early,
                           int64_t early_stride_b, const int32_t* rir_len, int32_t B, int32_t S, int32_t M,
                           int64_t R, int64_t F, float* h, void* stream);
+/* Hand-written FFT convolution of every filter row with its source (the
+   fftconvolve of mixture.py:216-218): uniformly partitioned overlap-save with
+   8192-point shared-memory FFTs (csrc/frir_fftconv.cu).  Inputs as for
+   frir_mix_pack_dry / frir_mix_pack_filters (placed speakers, tiled noise;
+   filter rows R taps); output y[b][j][y_stride] with rows j as for
+   frir_mix_combine, valid for t < T.  frir_mix_convolve_scratch returns the
+   scratch bytes (spectra) and the minimum y_stride. */
+int64_t frir_mix_convolve_scratch(int32_t B, int32_t S, int32_t M, int64_t R, int64_t T, int64_t* y_stride);
+int frir_mix_convolve(const float* dry, int64_t dry_stride_b, int64_t dry_stride_k, const float* noise,
+                      int64_t noise_stride, const int32_t* offsets, const int32_t* lengths, const int32_t* noise_len,
+                      const int32_t* dry_len, const float* rir_full, int64_t full_stride_b, const float* rir_early,
+                      int64_t early_stride_b, const int32_t* rir_len, int32_t B, int32_t S, int32_t M, int64_t R,
+                      int64_t T, void* scratch, int64_t scratch_bytes, float* y, int64_t y_stride, void* stream);
 /* _power (mixture.py:221-222): out[r] = mean(y[req_row[r]][req_lo[r]:req_hi[r]]^2),
    FP64, fixed-order sums; scratch holds FRIR_MIX_POWER_CHUNKS doubles per request. */
 #define FRIR_MIX_POWER_CHUNKS 32

@@ -108,6 +108,11 @@ SIGNATURES = [
     ("frir_mix_pack_filters", c_int32,
      [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int32, c_int32, c_int32, c_int64, c_int64, c_void_p,
       c_void_p]),
+    ("frir_mix_convolve_scratch", c_int64, [c_int32, c_int32, c_int32, c_int64, c_int64, ctypes.POINTER(c_int64)]),
+    ("frir_mix_convolve", c_int32,
+     [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64,
+      c_void_p, c_int64, c_void_p, c_int32, c_int32, c_int32, c_int64, c_int64, c_void_p, c_int64, c_void_p,
+      c_int64, c_void_p]),
     ("frir_mix_spectra", c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int64, c_void_p]),
     ("frir_mix_powers", c_int32,
      [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),

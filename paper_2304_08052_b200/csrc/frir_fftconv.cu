@@ -1,0 +1,374 @@
+// Hand-written FFT convolution for the spatialise-and-mix consumer (SURVEY
+// §8f row 1; reference framrir/mixture.py:216-218 _convolve_multichannel,
+// scipy fftconvolve): uniformly partitioned overlap-save with 8192-point
+// complex FFTs computed in shared memory.
+//
+//   block size P = 4096, FFT size N = 2P; the filter is cut into Q
+//   partitions of P taps, the input into blocks of P samples:
+//   y[tP + n] = last P samples of IFFT( sum_p X_{t-p} . H_p ),  n < P,
+//   X_s = FFT(x[(s-1)P, (s+1)P)),  H_p = FFT(h[pP, pP + P) zero-padded).
+//
+// Two real filter rows that share a source (speaker k: the full and early
+// filters of mic m; the noise: mics m, m+1) ride in one complex transform,
+// H = FFT(h_a + i h_b), so IFFT(X . H) = y_a + i y_b.  The FFT is a radix-8
+// (four passes) + radix-2 Stockham in place in 64 KB of shared memory, 512
+// threads, twiddles from an FP64-computed table.  FP32 throughout (the
+// reference is FP64; the mixing tests hold the result to 1e-5 of the peak).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/frir.h"
+#include "frir_internal.h"
+
+namespace frir {
+namespace {
+
+constexpr int kFftN = 8192;            // transform length
+constexpr int kFftP = kFftN / 2;       // hop / partition length
+constexpr int kFftThreads = 512;
+
+__device__ __forceinline__ float2 cmulf(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 addf(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 subf(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+// multiply by -i
+__device__ __forceinline__ float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }
+
+// Size-8 DFT in registers, natural order in and out (forward, W = e^{-2 pi i / 8}).
+__device__ __forceinline__ void dft8(float2 (&v)[8]) {
+  const float r = 0.70710678118654752f;
+  // span 4
+  float2 a0 = addf(v[0], v[4]), b0 = subf(v[0], v[4]);
+  float2 a1 = addf(v[1], v[5]), b1 = subf(v[1], v[5]);
+  float2 a2 = addf(v[2], v[6]), b2 = subf(v[2], v[6]);
+  float2 a3 = addf(v[3], v[7]), b3 = subf(v[3], v[7]);
+  b1 = make_float2(r * (b1.x + b1.y), r * (b1.y - b1.x));   // * W8^1
+  b2 = mul_mi(b2);                                          // * W8^2 = -i
+  b3 = make_float2(r * (b3.y - b3.x), -r * (b3.x + b3.y));  // * W8^3
+  // span 2
+  float2 c0 = addf(a0, a2), d0 = subf(a0, a2);
+  float2 c1 = addf(a1, a3), d1 = mul_mi(subf(a1, a3));
+  float2 e0 = addf(b0, b2), f0 = subf(b0, b2);
+  float2 e1 = addf(b1, b3), f1 = mul_mi(subf(b1, b3));
+  // span 1; outputs in bit-reversed positions -> natural order
+  v[0] = addf(c0, c1);
+  v[4] = subf(c0, c1);
+  v[2] = addf(d0, d1);
+  v[6] = subf(d0, d1);
+  v[1] = addf(e0, e1);
+  v[5] = subf(e0, e1);
+  v[3] = addf(f0, f1);
+  v[7] = subf(f0, f1);
+}
+
+// Shared-memory layout of the transform: one float2 of padding per 32
+// entries, so the stride-R / stride-Ns Stockham accesses spread over banks.
+__device__ __forceinline__ int pad(int i) { return i + (i >> 5); }
+constexpr int kFftPadded = kFftN + kFftN / 32;
+constexpr int kTwN = kFftN / 8;  // smem twiddle table: W^m, m < N / 8
+
+// One Stockham pass of radix R over buf (in place: every thread loads its
+// butterflies' inputs before the barrier, then stores).  NS = product of the
+// radices of the previous passes (compile time: divisions are shifts).
+// Twiddles W^{r k step}: w1 = W^{k step} from the smem table (k step < N/8,
+// times an eighth-circle rotation for the radix-2 pass), w_r = w1^r.
+template <int R, int NS>
+__device__ __forceinline__ void stockham_pass(float2* buf, const float2* tws) {
+  constexpr int NB = kFftN / R / kFftThreads;  // butterflies per thread
+  constexpr int step = kFftN / (NS * R);       // twiddle index stride
+  float2 v[NB][R];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int j = threadIdx.x + b * kFftThreads;
+    const int k = j & (NS - 1);
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[b][r] = buf[pad(j + r * (kFftN / R))];
+    if (NS > 1) {
+      const int m = k * step;  // < N / R
+      float2 w1;
+      if constexpr (R == 8) {
+        w1 = tws[m];
+      } else {  // m < N / 2: W^m = W^{m mod N/8} * e^{-i pi/4 * (m div N/8)}
+        const float2 lo = tws[m & (kTwN - 1)];
+        const int e = m / kTwN;  // 0..3
+        const float c = 0.70710678118654752f;
+        const float2 rot = e == 0 ? make_float2(1.f, 0.f)
+                         : e == 1 ? make_float2(c, -c)
+                         : e == 2 ? make_float2(0.f, -1.f) : make_float2(-c, -c);
+        w1 = cmulf(lo, rot);
+      }
+      float2 w = w1;
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        v[b][r] = cmulf(v[b][r], w);
+        if (r + 1 < R) w = cmulf(w, w1);
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int j = threadIdx.x + b * kFftThreads;
+    const int k = j & (NS - 1);
+    if constexpr (R == 8) {
+      dft8(v[b]);
+    } else {
+      const float2 a = v[b][0], c = v[b][1];
+      v[b][0] = addf(a, c);
+      v[b][1] = subf(a, c);
+    }
+    const int d = (j / NS) * NS * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) buf[pad(d + r * NS)] = v[b][r];
+  }
+  __syncthreads();
+}
+
+// Forward 8192-point FFT of buf (padded layout) in place (8 * 8 * 8 * 8 * 2).
+__device__ __forceinline__ void fft8192(float2* buf, const float2* tws) {
+  __syncthreads();
+  stockham_pass<8, 1>(buf, tws);
+  stockham_pass<8, 8>(buf, tws);
+  stockham_pass<8, 64>(buf, tws);
+  stockham_pass<8, 512>(buf, tws);
+  stockham_pass<2, 4096>(buf, tws);
+}
+
+// Shared memory of the FFT kernels: the padded transform, then the twiddles.
+__device__ __forceinline__ float2* load_twiddles(float2* smem_base, const float2* __restrict__ tw) {
+  float2* tws = smem_base + kFftPadded;
+  for (int i = threadIdx.x; i < kTwN; i += kFftThreads) tws[i] = __ldg(tw + i);
+  return tws;
+}
+constexpr size_t kFftSmem = (size_t)(kFftPadded + kTwN) * sizeof(float2);
+
+struct ConvArgs {
+  const float* dry;
+  long dry_sb, dry_sk;
+  const float* noise;
+  long noise_sb;
+  const int32_t* off;
+  const int32_t* len;
+  const int32_t* nlen;
+  const int32_t* dlen;
+  const float* rir_full;
+  long full_sb;
+  const float* rir_early;
+  long early_sb;
+  const int32_t* rlen;
+  int S, M, R, nb, Q, npairs;
+  const float2* tw;
+  float2* X;   // [B][S+1][nb][N]
+  float2* H;   // [B][npairs][Q][N]
+  float* y;    // [B][J][y_stride]
+  long y_stride;
+};
+
+// pair -> (row a, row b or -1, source)
+__device__ __forceinline__ void pair_rows(int pi, int S, int M, int* ja, int* jb, int* src) {
+  if (pi < S * M) {
+    const int k = pi / M, m = pi % M;
+    *ja = k * M + m;          // full filter, speaker k, mic m
+    *jb = (S + k) * M + m;    // early filter
+    *src = k;
+  } else {
+    const int m = 2 * (pi - S * M);
+    *ja = 2 * S * M + m;      // noise filters, mics m and m + 1
+    *jb = m + 1 < M ? 2 * S * M + m + 1 : -1;
+    *src = S;
+  }
+}
+
+// X_t = FFT of the placed dry signal (speaker k at its offset, or the tiled
+// noise) over [(t-1)P, (t+1)P).  Grid (nb, S+1, B).
+__global__ void __launch_bounds__(kFftThreads, 2) fft_in_kernel(ConvArgs A) {
+  extern __shared__ __align__(16) float2 buf[];
+  const int t = blockIdx.x, k = blockIdx.y, b = blockIdx.z;
+  const float2* tws = load_twiddles(buf, A.tw);
+  const long base = (long)(t - 1) * kFftP;
+  if (k < A.S) {
+    const long o = A.off[b * A.S + k], n = A.len[b * A.S + k];
+    const float* src = A.dry + (size_t)b * A.dry_sb + (size_t)k * A.dry_sk;
+    for (int u = threadIdx.x; u < kFftN; u += kFftThreads) {
+      const long q = base + u - o;
+      buf[pad(u)] = make_float2(q >= 0 && q < n ? __ldg(src + q) : 0.f, 0.f);
+    }
+  } else {  // the point noise tiled to the dry length
+    const long dl = A.dlen[b], nl = A.nlen[b];
+    const float* src = A.noise + (size_t)b * A.noise_sb;
+    long pos = base + threadIdx.x;
+    long q = pos >= 0 ? pos % nl : 0;
+    for (int u = threadIdx.x; u < kFftN; u += kFftThreads, pos += kFftThreads) {
+      buf[pad(u)] = make_float2(pos >= 0 && pos < dl ? __ldg(src + q) : 0.f, 0.f);
+      if (pos >= 0) {
+        q += kFftThreads;
+        while (q >= nl) q -= nl;
+      } else if (pos + kFftThreads >= 0) {
+        q = (pos + kFftThreads) % nl;
+      }
+    }
+  }
+  fft8192(buf, tws);
+  float2* out = A.X + (((size_t)b * (A.S + 1) + k) * A.nb + t) * kFftN;
+  for (int f = threadIdx.x; f < kFftN; f += kFftThreads) out[f] = buf[pad(f)];
+}
+
+// H_p = FFT(h_a + i h_b) over taps [pP, pP + P).  Grid (Q, npairs, B).
+__global__ void __launch_bounds__(kFftThreads, 2) fft_filt_kernel(ConvArgs A) {
+  extern __shared__ __align__(16) float2 buf[];
+  const int p = blockIdx.x, pi = blockIdx.y, b = blockIdx.z;
+  const int M = A.M, S = A.S, r = A.rlen[b];
+  if (p * kFftP >= r) return;  // partitions past this item's filter length are never read
+  int ja, jb, src;
+  pair_rows(pi, A.S, A.M, &ja, &jb, &src);
+  auto row = [&](int j) -> const float* {
+    if (j < S * M) return A.rir_full + (size_t)b * A.full_sb + (size_t)j * A.R;
+    if (j < 2 * S * M) {
+      const int jj = j - S * M;
+      return A.rir_early ? A.rir_early + (size_t)b * A.early_sb + (size_t)jj * A.R
+                         : A.rir_full + (size_t)b * A.full_sb + (size_t)jj * A.R;
+    }
+    return A.rir_full + (size_t)b * A.full_sb + ((size_t)S * M + (j - 2 * S * M)) * A.R;
+  };
+  const float* ha = row(ja);
+  const float* hb = jb >= 0 ? row(jb) : nullptr;
+  const float2* tws = load_twiddles(buf, A.tw);
+  for (int u = threadIdx.x; u < kFftN; u += kFftThreads) {
+    const int tap = p * kFftP + u;
+    float va = 0.f, vb = 0.f;
+    if (u < kFftP && tap < r) {
+      va = __ldg(ha + tap);
+      if (hb) vb = __ldg(hb + tap);
+    }
+    buf[pad(u)] = make_float2(va, vb);
+  }
+  fft8192(buf, tws);
+  float2* out = A.H + (((size_t)b * A.npairs + pi) * A.Q + p) * kFftN;
+  for (int f = threadIdx.x; f < kFftN; f += kFftThreads) out[f] = buf[pad(f)];
+}
+
+// Output block t of a pair: sum_p X_{t-p} H_p, inverse FFT (conj trick),
+// last P samples -> y_a (real), y_b (imag).  Grid (nb, npairs, B).
+__global__ void __launch_bounds__(kFftThreads, 2) fft_conv_kernel(ConvArgs A) {
+  extern __shared__ __align__(16) float2 buf[];
+  const int t = blockIdx.x, pi = blockIdx.y, b = blockIdx.z;
+  int ja, jb, src;
+  pair_rows(pi, A.S, A.M, &ja, &jb, &src);
+  const float2* Xs = A.X + ((size_t)b * (A.S + 1) + src) * A.nb * kFftN;
+  const float2* Hs = A.H + ((size_t)b * A.npairs + pi) * A.Q * kFftN;
+  const int qb = (A.rlen[b] + kFftP - 1) / kFftP;  // this item's non-zero partitions
+  const int qmax = min(qb - 1, t);
+  const float2* tws = load_twiddles(buf, A.tw);
+  for (int f = threadIdx.x; f < kFftN; f += kFftThreads) {
+    float2 acc = make_float2(0.f, 0.f);
+    for (int p = 0; p <= qmax; ++p) {
+      const float2 x = __ldg(Xs + (size_t)(t - p) * kFftN + f), h = __ldg(Hs + (size_t)p * kFftN + f);
+      acc.x = fmaf(x.x, h.x, fmaf(-x.y, h.y, acc.x));
+      acc.y = fmaf(x.x, h.y, fmaf(x.y, h.x, acc.y));
+    }
+    buf[pad(f)] = make_float2(acc.x, -acc.y);  // conj: IFFT(z) = conj(FFT(conj(z))) / N
+  }
+  fft8192(buf, tws);
+  const float inv = 1.0f / kFftN;
+  float* ya = A.y + ((size_t)b * ((2 * A.S + 1) * A.M) + ja) * A.y_stride + (size_t)t * kFftP;
+  float* yb = jb >= 0 ? A.y + ((size_t)b * ((2 * A.S + 1) * A.M) + jb) * A.y_stride + (size_t)t * kFftP : nullptr;
+  for (int n = threadIdx.x; n < kFftP; n += kFftThreads) {
+    const float2 z = buf[pad(kFftP + n)];
+    ya[n] = z.x * inv;
+    if (yb) yb[n] = -z.y * inv;
+  }
+}
+
+// Twiddle table exp(-2 pi i m / N), m < N, per device (FP64-computed).
+const float2* twiddles(std::string* err) {
+  static std::mutex mu;
+  static const float2* tab[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  if (dev < 0 || dev >= 64) { *err = "device index out of range"; return nullptr; }
+  if (!tab[dev]) {
+    std::vector<float2> h(kFftN);
+    for (int m = 0; m < kFftN; ++m) {
+      const double a = -2.0 * M_PI * (double)m / (double)kFftN;
+      h[m] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+    float2* d = nullptr;
+    cudaError_t e = cudaMalloc((void**)&d, kFftN * sizeof(float2));
+    if (e == cudaSuccess) e = cudaMemcpy(d, h.data(), kFftN * sizeof(float2), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { *err = cudaGetErrorString(e); return nullptr; }
+    tab[dev] = d;
+  }
+  return tab[dev];
+}
+
+}  // namespace
+}  // namespace frir
+
+using namespace frir;
+
+extern "C" {
+
+int64_t frir_mix_convolve_scratch(int32_t B, int32_t S, int32_t M, int64_t R, int64_t T, int64_t* y_stride) {
+  if (B < 0 || S < 1 || M < 1 || R < 1 || T < 1) return -1;
+  const int64_t nb = (T + kFftP - 1) / kFftP;
+  const int64_t Q = (R + kFftP - 1) / kFftP;
+  const int64_t npairs = (int64_t)S * M + (M + 1) / 2;
+  if (y_stride) *y_stride = nb * kFftP;
+  return ((int64_t)B * (S + 1) * nb + (int64_t)B * npairs * Q) * kFftN * (int64_t)sizeof(float2);
+}
+
+int frir_mix_convolve(const float* dry, int64_t dry_stride_b, int64_t dry_stride_k, const float* noise,
+                      int64_t noise_stride, const int32_t* offsets, const int32_t* lengths, const int32_t* noise_len,
+                      const int32_t* dry_len, const float* rir_full, int64_t full_stride_b, const float* rir_early,
+                      int64_t early_stride_b, const int32_t* rir_len, int32_t B, int32_t S, int32_t M, int64_t R,
+                      int64_t T, void* scratch, int64_t scratch_bytes, float* y, int64_t y_stride, void* stream) {
+  int64_t ys = 0;
+  const int64_t need = frir_mix_convolve_scratch(B, S, M, R, T, &ys);
+  if (!dry || !noise || !offsets || !lengths || !noise_len || !dry_len || !rir_full || !rir_len || !scratch || !y ||
+      need < 0 || scratch_bytes < need || y_stride < ys) {
+    set_error("frir_mix_convolve: invalid argument or scratch/y too small");
+    return FRIR_EINVAL;
+  }
+  if (B == 0) return FRIR_OK;
+  std::string err;
+  const float2* tw = twiddles(&err);
+  if (!tw) { set_error("frir_mix_convolve: " + err); return FRIR_ECUDA; }
+  ConvArgs a;
+  a.dry = dry; a.dry_sb = (long)dry_stride_b; a.dry_sk = (long)dry_stride_k;
+  a.noise = noise; a.noise_sb = (long)noise_stride;
+  a.off = offsets; a.len = lengths; a.nlen = noise_len; a.dlen = dry_len;
+  a.rir_full = rir_full; a.full_sb = (long)full_stride_b; a.rir_early = rir_early; a.early_sb = (long)early_stride_b;
+  a.rlen = rir_len;
+  a.S = S; a.M = M; a.R = (int)R;
+  a.nb = (int)((T + kFftP - 1) / kFftP);
+  a.Q = (int)((R + kFftP - 1) / kFftP);
+  a.npairs = S * M + (M + 1) / 2;
+  a.tw = tw;
+  a.X = (float2*)scratch;
+  a.H = a.X + (size_t)B * (S + 1) * a.nb * kFftN;
+  a.y = y; a.y_stride = (long)y_stride;
+  const size_t smem = kFftSmem;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaSuccess;
+  for (auto k : {(const void*)fft_in_kernel, (const void*)fft_filt_kernel, (const void*)fft_conv_kernel}) {
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) break;
+  }
+  if (e == cudaSuccess) {
+    fft_in_kernel<<<dim3(a.nb, S + 1, B), kFftThreads, smem, st>>>(a);
+    fft_filt_kernel<<<dim3(a.Q, a.npairs, B), kFftThreads, smem, st>>>(a);
+    fft_conv_kernel<<<dim3(a.nb, a.npairs, B), kFftThreads, smem, st>>>(a);
+    e = cudaGetLastError();
+  }
+  if (e != cudaSuccess) { set_error(std::string("frir_mix_convolve: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
+  return FRIR_OK;
+}
+
+}  // extern "C"

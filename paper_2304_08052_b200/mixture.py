@@ -18,6 +18,7 @@ drop-in for one utterance with numpy in and out.
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass, replace
 
@@ -207,8 +208,6 @@ def mix_device(dry, dry_len, offsets, noise, noise_len, rir_full, rir_early, rir
     rir_len = np.asarray(rir_len, dtype=np.int64).reshape(B)
     total = (offsets + dry_len).max(axis=1) + rir_len - 1          # mixture.py:272
     T = int(total.max()) if B else 0
-    F = fft_size(T)
-    Fc = F // 2 + 1
     lib = _abi.lib()
     stream = torch.cuda.current_stream(dev).cuda_stream
 
@@ -223,32 +222,24 @@ def mix_device(dry, dry_len, offsets, noise, noise_len, rir_full, rir_early, rir
         raise ValueError("rir_early must be (B, >= S, M, R) like rir_full")
     if rir_early is not None and rir_early.stride()[1:] != (M * R, R, 1):
         rir_early = rir_early.contiguous()
-    # dry signals at their offsets, then the point noise tiled to the dry length (:307-312)
+    # convolution of every filter row with its source: libfrir's hand-written
+    # partitioned overlap-save FFT convolution (placed speakers, tiled noise)
     dlen = total - rir_len + 1
-    x = torch.empty((B, S + 1, F), dtype=torch.float32, device=dev)
-    # (device copies held in locals: a temporary's memory could be reused before the launch)
     off_d, len_d, nlen_d, dlen_d = i32(offsets), i32(dry_len), i32(noise_len), i32(dlen)
-    _abi.check(lib.frir_mix_pack_dry(dry.data_ptr(), dry.stride(0), dry.stride(1), noise.data_ptr(),
-                                     noise.stride(0), off_d.data_ptr(), len_d.data_ptr(), nlen_d.data_ptr(),
-                                     dlen_d.data_ptr(), B, S, F, x.data_ptr(), stream), "frir_mix_pack_dry")
-    # filter rows: kM+m full of speaker k, (S+k)M+m early, 2SM+m noise
-    J = (2 * S + 1) * M
-    h = torch.empty((B, J, F), dtype=torch.float32, device=dev)
     rl = i32(rir_len)
-    _abi.check(lib.frir_mix_pack_filters(rir_full.data_ptr(), rir_full.stride(0),
-                                         rir_early.data_ptr() if rir_early is not None else None,
-                                         rir_early.stride(0) if rir_early is not None else 0,
-                                         rl.data_ptr(), B, S, M, R, F, h.data_ptr(), stream),
-               "frir_mix_pack_filters")
-    src_of = torch.tensor(np.concatenate([np.repeat(np.arange(S), M), np.repeat(np.arange(S), M),
-                                          np.full(M, S)]).astype(np.int32), device=dev)
-    X = torch.fft.rfft(x, n=F)
-    H = torch.fft.rfft(h, n=F)
-    del x, h
-    _abi.check(lib.frir_mix_spectra(H.data_ptr(), X.data_ptr(), src_of.data_ptr(), B, J, S + 1, Fc,
-                                    stream), "frir_mix_spectra")
-    y = torch.fft.irfft(H, n=F)
-    del H, X
+    J = (2 * S + 1) * M
+    ys = ctypes.c_int64(0)
+    nscr = lib.frir_mix_convolve_scratch(B, S, M, R, T, ctypes.byref(ys))
+    F = int(ys.value)  # row stride of y
+    scratch = torch.empty(max(int(nscr), 1), dtype=torch.uint8, device=dev)
+    y = torch.empty((B, J, F), dtype=torch.float32, device=dev)
+    _abi.check(lib.frir_mix_convolve(
+        dry.data_ptr(), dry.stride(0), dry.stride(1), noise.data_ptr(), noise.stride(0), off_d.data_ptr(),
+        len_d.data_ptr(), nlen_d.data_ptr(), dlen_d.data_ptr(), rir_full.data_ptr(), rir_full.stride(0),
+        rir_early.data_ptr() if rir_early is not None else None, rir_early.stride(0) if rir_early is not None else 0,
+        rl.data_ptr(), B, S, M, R, T, scratch.data_ptr(), scratch.numel(), y.data_ptr(), F, stream),
+        "frir_mix_convolve")
+    del scratch
 
     # reference-channel power requests (mixture.py:284-303, 311), per item:
     # p_ref, (p_int_k, p_tgt_k) for k = 1..S-1, p_noise
