@@ -206,32 +206,18 @@ int frir_simulate_stages(const frir_plan* plan, const frir_batch* batch, void* w
 int32_t frir_launch_count(const frir_plan* plan, const frir_batch* batch, int32_t early);
 
 /* ---- spatialise-and-mix consumer (mixture.py:216-332) ----
-   The batched FFT convolution runs in cuFFT on the caller's side; these are
-   the kernels around it.  All pointers are device pointers.
+   All pointers are device pointers. */
 
-   Spectral products of _convolve_multichannel (mixture.py:216-218):
-   filt_spec[b][j][f] *= dry_spec[b][src_of[j]][f]  (complex64, f < Fc). */
-int frir_mix_spectra(void* filt_spec, const void* dry_spec, const int32_t* src_of, int32_t B,
-                     int32_t J, int32_t K, int64_t Fc, void* stream);
-/* FFT frames of the dry signals (mixture.py:274-287, 307-312): x[b][k][F] for
-   k < S holds speaker k at offsets[b][k] (lengths[b][k] samples of dry), k = S
-   the noise tiled to dry_len[b] samples; zeros elsewhere. */
-int frir_mix_pack_dry(const float* dry, int64_t dry_stride_b, int64_t dry_stride_k, const float* noise,
-                      int64_t noise_stride, const int32_t* offsets, const int32_t* lengths,
-                      const int32_t* noise_len, const int32_t* dry_len, int32_t B, int32_t S, int64_t F,
-                      float* x, void* stream);
-/* FFT frames of the filters: h[b][j][F], rows j = kM+m (full, speaker k),
-   (S+k)M+m (early; full when rir_early is NULL), 2SM+m (noise); item b's
-   filters are [S+1][M][R] at rir_full + b*full_stride_b and [>= S][M][R] at
-   rir_early + b*early_stride_b (floats); rir_len[b] valid taps. */
-int frir_mix_pack_filters(const float* rir_full, int64_t full_stride_b, const float* rir_early,
-                          int64_t early_stride_b, const int32_t* rir_len, int32_t B, int32_t S, int32_t M,
-                          int64_t R, int64_t F, float* h, void* stream);
 /* Hand-written FFT convolution of every filter row with its source (the
    fftconvolve of mixture.py:216-218): uniformly partitioned overlap-save with
-   8192-point shared-memory FFTs (csrc/frir_fftconv.cu).  Inputs as for
-   frir_mix_pack_dry / frir_mix_pack_filters (placed speakers, tiled noise;
-   filter rows R taps); output y[b][j][y_stride] with rows j as for
+   8192-point shared-memory FFTs (csrc/frir_fftconv.cu).  Sources: speaker k
+   of item b is dry[b*dry_stride_b + k*dry_stride_k + 0 .. lengths[b][k]),
+   placed at offsets[b][k] (mixture.py:274-287); the point noise
+   noise[b*noise_stride ..] tiled to dry_len[b] samples (noise_len[b] long,
+   mixture.py:307-312).  Filters: item b's [S+1][M][R] full rows at
+   rir_full + b*full_stride_b and [>= S][M][R] early rows at rir_early +
+   b*early_stride_b (full when rir_early is NULL), rir_len[b] valid taps.
+   Output y[b][j][y_stride] with rows j as for
    frir_mix_combine, valid for t < T.  frir_mix_convolve_scratch returns the
    scratch bytes (spectra) and the minimum y_stride. */
 int64_t frir_mix_convolve_scratch(int32_t B, int32_t S, int32_t M, int64_t R, int64_t T, int64_t* y_stride);

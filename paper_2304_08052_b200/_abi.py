@@ -102,18 +102,11 @@ SIGNATURES = [
      [c_void_p, ctypes.POINTER(FrirBatch), c_void_p, ctypes.c_size_t, c_void_p, c_void_p,
       c_void_p, c_void_p, c_int32]),
     ("frir_launch_count", c_int32, [c_void_p, ctypes.POINTER(FrirBatch), c_int32]),
-    ("frir_mix_pack_dry", c_int32,
-     [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int32,
-      c_int32, c_int64, c_void_p, c_void_p]),
-    ("frir_mix_pack_filters", c_int32,
-     [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int32, c_int32, c_int32, c_int64, c_int64, c_void_p,
-      c_void_p]),
     ("frir_mix_convolve_scratch", c_int64, [c_int32, c_int32, c_int32, c_int64, c_int64, ctypes.POINTER(c_int64)]),
     ("frir_mix_convolve", c_int32,
      [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64,
       c_void_p, c_int64, c_void_p, c_int32, c_int32, c_int32, c_int64, c_int64, c_void_p, c_int64, c_void_p,
       c_int64, c_void_p]),
-    ("frir_mix_spectra", c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int64, c_void_p]),
     ("frir_mix_powers", c_int32,
      [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
     ("frir_mix_gains", c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p]),

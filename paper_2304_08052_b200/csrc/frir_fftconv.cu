@@ -73,6 +73,18 @@ __device__ __forceinline__ int pad(int i) { return i + (i >> 5); }
 constexpr int kFftPadded = kFftN + kFftN / 32;
 constexpr int kTwN = kFftN / 8;  // smem twiddle table: W^m, m < N / 8
 
+// W^m for m < N / 2 from the eighth-circle table: W^{m mod N/8} times the
+// rotation e^{-i pi/4 * (m div N/8)}.
+__device__ __forceinline__ float2 twiddle_half(const float2* tws, int m) {
+  const float2 lo = tws[m & (kTwN - 1)];
+  const int e = m / kTwN;  // 0..3
+  const float c = 0.70710678118654752f;
+  const float2 rot = e == 0 ? make_float2(1.f, 0.f)
+                   : e == 1 ? make_float2(c, -c)
+                   : e == 2 ? make_float2(0.f, -1.f) : make_float2(-c, -c);
+  return cmulf(lo, rot);
+}
+
 // One Stockham pass of radix R over buf (in place: every thread loads its
 // butterflies' inputs before the barrier, then stores).  NS = product of the
 // radices of the previous passes (compile time: divisions are shifts).
@@ -91,18 +103,7 @@ __device__ __forceinline__ void stockham_pass(float2* buf, const float2* tws) {
     for (int r = 0; r < R; ++r) v[b][r] = buf[pad(j + r * (kFftN / R))];
     if (NS > 1) {
       const int m = k * step;  // < N / R
-      float2 w1;
-      if constexpr (R == 8) {
-        w1 = tws[m];
-      } else {  // m < N / 2: W^m = W^{m mod N/8} * e^{-i pi/4 * (m div N/8)}
-        const float2 lo = tws[m & (kTwN - 1)];
-        const int e = m / kTwN;  // 0..3
-        const float c = 0.70710678118654752f;
-        const float2 rot = e == 0 ? make_float2(1.f, 0.f)
-                         : e == 1 ? make_float2(c, -c)
-                         : e == 2 ? make_float2(0.f, -1.f) : make_float2(-c, -c);
-        w1 = cmulf(lo, rot);
-      }
+      const float2 w1 = R == 8 ? tws[m] : twiddle_half(tws, m);
       float2 w = w1;
 #pragma unroll
       for (int r = 1; r < R; ++r) {
@@ -130,14 +131,30 @@ __device__ __forceinline__ void stockham_pass(float2* buf, const float2* tws) {
   __syncthreads();
 }
 
-// Forward 8192-point FFT of buf (padded layout) in place (8 * 8 * 8 * 8 * 2).
-__device__ __forceinline__ void fft8192(float2* buf, const float2* tws) {
+// The forward 8192-point FFT (8 * 8 * 8 * 8 * 2) in three pieces so the
+// kernels feed the first pass from registers and take the last pass's outputs
+// straight to global memory (no shared-memory round trip at either end):
+//   fft_first(buf, v, j): pass 1 (radix 8, no twiddles) of butterfly j < N/8,
+//     v[r] = x[j + r N/8]; results to buf.
+//   fft_mid(buf, tws): passes 2-4 (after a barrier; ends with one).
+//   fft_last(buf, tws, j, ...): pass 5 (radix 2) of butterfly j < N/2 ->
+//     X[j], X[j + N/2].
+__device__ __forceinline__ void fft_first(float2* buf, float2 (&v)[8], int j) {
+  dft8(v);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) buf[pad(8 * j + r)] = v[r];
+}
+__device__ __forceinline__ void fft_mid(float2* buf, const float2* tws) {
   __syncthreads();
-  stockham_pass<8, 1>(buf, tws);
   stockham_pass<8, 8>(buf, tws);
   stockham_pass<8, 64>(buf, tws);
   stockham_pass<8, 512>(buf, tws);
-  stockham_pass<2, 4096>(buf, tws);
+}
+__device__ __forceinline__ void fft_last(const float2* buf, const float2* tws, int j, float2* x0, float2* x1) {
+  const float2 a = buf[pad(j)];
+  const float2 c = cmulf(buf[pad(j + kFftP)], twiddle_half(tws, j));
+  *x0 = addf(a, c);
+  *x1 = subf(a, c);
 }
 
 // Shared memory of the FFT kernels: the padded transform, then the twiddles.
@@ -192,20 +209,23 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_in_kernel(ConvArgs A) {
   const int t = blockIdx.x, k = blockIdx.y, b = blockIdx.z;
   const float2* tws = load_twiddles(buf, A.tw);
   const long base = (long)(t - 1) * kFftP;
+  float vals[kFftN / kFftThreads];  // samples base + threadIdx.x + i * 512
   if (k < A.S) {
     const long o = A.off[b * A.S + k], n = A.len[b * A.S + k];
     const float* src = A.dry + (size_t)b * A.dry_sb + (size_t)k * A.dry_sk;
-    for (int u = threadIdx.x; u < kFftN; u += kFftThreads) {
-      const long q = base + u - o;
-      buf[pad(u)] = make_float2(q >= 0 && q < n ? __ldg(src + q) : 0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < kFftN / kFftThreads; ++i) {
+      const long q = base + threadIdx.x + i * kFftThreads - o;
+      vals[i] = q >= 0 && q < n ? __ldg(src + q) : 0.f;
     }
   } else {  // the point noise tiled to the dry length
     const long dl = A.dlen[b], nl = A.nlen[b];
     const float* src = A.noise + (size_t)b * A.noise_sb;
     long pos = base + threadIdx.x;
     long q = pos >= 0 ? pos % nl : 0;
-    for (int u = threadIdx.x; u < kFftN; u += kFftThreads, pos += kFftThreads) {
-      buf[pad(u)] = make_float2(pos >= 0 && pos < dl ? __ldg(src + q) : 0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < kFftN / kFftThreads; ++i, pos += kFftThreads) {
+      vals[i] = pos >= 0 && pos < dl ? __ldg(src + q) : 0.f;
       if (pos >= 0) {
         q += kFftThreads;
         while (q >= nl) q -= nl;
@@ -214,9 +234,16 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_in_kernel(ConvArgs A) {
       }
     }
   }
-  fft8192(buf, tws);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {  // butterflies j = threadIdx.x + h * 512 read samples j + r * 1024
+    float2 v[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = make_float2(vals[h + 2 * r], 0.f);
+    fft_first(buf, v, threadIdx.x + h * kFftThreads);
+  }
+  fft_mid(buf, tws);
   float2* out = A.X + (((size_t)b * (A.S + 1) + k) * A.nb + t) * kFftN;
-  for (int f = threadIdx.x; f < kFftN; f += kFftThreads) out[f] = buf[pad(f)];
+  for (int j = threadIdx.x; j < kFftP; j += kFftThreads) fft_last(buf, tws, j, out + j, out + j + kFftP);
 }
 
 // H_p = FFT(h_a + i h_b) over taps [pP, pP + P).  Grid (Q, npairs, B).
@@ -239,18 +266,25 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_filt_kernel(ConvArgs A) {
   const float* ha = row(ja);
   const float* hb = jb >= 0 ? row(jb) : nullptr;
   const float2* tws = load_twiddles(buf, A.tw);
-  for (int u = threadIdx.x; u < kFftN; u += kFftThreads) {
-    const int tap = p * kFftP + u;
-    float va = 0.f, vb = 0.f;
-    if (u < kFftP && tap < r) {
-      va = __ldg(ha + tap);
-      if (hb) vb = __ldg(hb + tap);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int j = threadIdx.x + h * kFftThreads;
+    float2 v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {  // taps j + q * 1024 of the partition; the upper half is padding
+      const int u = j + q * (kFftN / 8), tap = p * kFftP + u;
+      float va = 0.f, vb = 0.f;
+      if (u < kFftP && tap < r) {
+        va = __ldg(ha + tap);
+        if (hb) vb = __ldg(hb + tap);
+      }
+      v[q] = make_float2(va, vb);
     }
-    buf[pad(u)] = make_float2(va, vb);
+    fft_first(buf, v, j);
   }
-  fft8192(buf, tws);
+  fft_mid(buf, tws);
   float2* out = A.H + (((size_t)b * A.npairs + pi) * A.Q + p) * kFftN;
-  for (int f = threadIdx.x; f < kFftN; f += kFftThreads) out[f] = buf[pad(f)];
+  for (int j = threadIdx.x; j < kFftP; j += kFftThreads) fft_last(buf, tws, j, out + j, out + j + kFftP);
 }
 
 // Output block t of a pair: sum_p X_{t-p} H_p, inverse FFT (conj trick),
@@ -265,23 +299,40 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_conv_kernel(ConvArgs A) {
   const int qb = (A.rlen[b] + kFftP - 1) / kFftP;  // this item's non-zero partitions
   const int qmax = min(qb - 1, t);
   const float2* tws = load_twiddles(buf, A.tw);
-  for (int f = threadIdx.x; f < kFftN; f += kFftThreads) {
-    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {  // butterfly j of pass 1 reads bins j + r * 1024
+    const int j = threadIdx.x + h * kFftThreads;
+    float2 v[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r] = make_float2(0.f, 0.f);
     for (int p = 0; p <= qmax; ++p) {
-      const float2 x = __ldg(Xs + (size_t)(t - p) * kFftN + f), h = __ldg(Hs + (size_t)p * kFftN + f);
-      acc.x = fmaf(x.x, h.x, fmaf(-x.y, h.y, acc.x));
-      acc.y = fmaf(x.x, h.y, fmaf(x.y, h.x, acc.y));
+      const float2* xp = Xs + (size_t)(t - p) * kFftN + j;
+      const float2* hp = Hs + (size_t)p * kFftN + j;
+      float2 x[8], hh[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        x[r] = __ldg(xp + r * (kFftN / 8));
+        hh[r] = __ldg(hp + r * (kFftN / 8));
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        v[r].x = fmaf(x[r].x, hh[r].x, fmaf(-x[r].y, hh[r].y, v[r].x));
+        v[r].y = fmaf(x[r].x, hh[r].y, fmaf(x[r].y, hh[r].x, v[r].y));
+      }
     }
-    buf[pad(f)] = make_float2(acc.x, -acc.y);  // conj: IFFT(z) = conj(FFT(conj(z))) / N
+#pragma unroll
+    for (int r = 0; r < 8; ++r) v[r].y = -v[r].y;  // conj: IFFT(z) = conj(FFT(conj(z))) / N
+    fft_first(buf, v, j);
   }
-  fft8192(buf, tws);
+  fft_mid(buf, tws);
   const float inv = 1.0f / kFftN;
   float* ya = A.y + ((size_t)b * ((2 * A.S + 1) * A.M) + ja) * A.y_stride + (size_t)t * kFftP;
   float* yb = jb >= 0 ? A.y + ((size_t)b * ((2 * A.S + 1) * A.M) + jb) * A.y_stride + (size_t)t * kFftP : nullptr;
-  for (int n = threadIdx.x; n < kFftP; n += kFftThreads) {
-    const float2 z = buf[pad(kFftP + n)];
-    ya[n] = z.x * inv;
-    if (yb) yb[n] = -z.y * inv;
+  for (int n = threadIdx.x; n < kFftP; n += kFftThreads) {  // the last P outputs: X[n + P]
+    float2 z0, z1;
+    fft_last(buf, tws, n, &z0, &z1);
+    ya[n] = z1.x * inv;
+    if (yb) yb[n] = -z1.y * inv;
   }
 }
 

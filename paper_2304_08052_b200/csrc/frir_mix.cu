@@ -1,9 +1,8 @@
 // sm_100a kernels of the spatialise-and-mix consumer:
 // reference framrir/mixture.py:216-222 (_convolve_multichannel, _power) and
-// :225-332 (spatialize_and_mix).  The FFTs of the batched convolution run in
-// cuFFT (through torch on the host side); these kernels do everything around
-// them: the per-filter spectral products, the reference-channel powers, the
-// SIR/SNR gains and the scaled outputs plus the mixture.  FP32 samples, FP64
+// :225-332 (spatialize_and_mix).  The batched convolution itself is
+// frir_fftconv.cu; these kernels do everything after it: the reference-channel
+// powers, the SIR/SNR gains and the scaled outputs plus the mixture.  FP32 samples, FP64
 // powers and gains (the reference computes in FP64), fixed-order reductions.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -16,19 +15,6 @@
 
 namespace frir {
 namespace {
-
-// spec[b][j][f] *= dry[b][src_of[j]][f], complex64 interleaved, f < Fc.
-// Grid (f blocks, J, B): one filter row per (y, z).
-__global__ void mix_spectra_kernel(float2* __restrict__ spec, const float2* __restrict__ dry,
-                                   const int32_t* __restrict__ src_of, int J, int K, long Fc) {
-  const int j = blockIdx.y, b = blockIdx.z;
-  float2* s = spec + ((size_t)b * J + j) * Fc;
-  const float2* x = dry + ((size_t)b * K + src_of[j]) * Fc;
-  for (long f = blockIdx.x * (long)blockDim.x + threadIdx.x; f < Fc; f += (long)gridDim.x * blockDim.x) {
-    const float2 h = s[f], d = __ldg(x + f);
-    s[f] = make_float2(h.x * d.x - h.y * d.y, h.x * d.y + h.y * d.x);
-  }
-}
 
 // Sums of squares over [lo, hi) of one row per request, split into kPowChunks
 // chunks (grid (chunks, requests)); FP64, fixed order: each chunk's block
@@ -116,55 +102,6 @@ __global__ void mix_combine_kernel(const float* __restrict__ y, const double* __
   }
 }
 
-// Dry signals of one FFT frame per (item, source): speakers at their offsets,
-// the point noise tiled to the dry length (mixture.py:307-312).
-// x[b][k][t], k < S: dry[b][k][t - off[b][k]] inside [0, len), else 0;
-// x[b][S][t] = noise[b][t mod nlen[b]] for t < dlen[b], else 0.
-__global__ void mix_pack_dry_kernel(const float* __restrict__ dry, long dry_stride_b, long dry_stride_k,
-                                    const float* __restrict__ noise, long noise_stride,
-                                    const int32_t* __restrict__ off, const int32_t* __restrict__ len,
-                                    const int32_t* __restrict__ nlen, const int32_t* __restrict__ dlen,
-                                    int S, long F, float* __restrict__ x) {
-  const int b = blockIdx.z, k = blockIdx.y;
-  float* row = x + ((size_t)b * (S + 1) + k) * F;
-  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < F; t += (long)gridDim.x * blockDim.x) {
-    float v = 0.f;
-    if (k < S) {
-      const long u = t - off[b * S + k];
-      if (u >= 0 && u < len[b * S + k]) v = dry[(size_t)b * dry_stride_b + (size_t)k * dry_stride_k + u];
-    } else if (t < dlen[b]) {
-      v = noise[(size_t)b * noise_stride + t % nlen[b]];
-    }
-    row[t] = v;
-  }
-}
-
-// Filter rows of one FFT frame each: h[b][j][t] for t < rlen[b] (zero after):
-// j = kM+m full of speaker k, (S+k)M+m early (full when early == nullptr),
-// 2SM+m the noise filter.  Per item b, rir_full + b * full_sb is [S+1][M][R]
-// and rir_early + b * early_sb is [>= S][M][R].
-__global__ void mix_pack_filters_kernel(const float* __restrict__ rir_full, long full_sb,
-                                        const float* __restrict__ rir_early, long early_sb,
-                                        const int32_t* __restrict__ rlen, int S, int M, long R, long F,
-                                        float* __restrict__ h) {
-  const int b = blockIdx.z, j = blockIdx.y;
-  const int J = (2 * S + 1) * M;
-  float* row = h + ((size_t)b * J + j) * F;
-  const float* src;
-  if (j < S * M) {
-    src = rir_full + (size_t)b * full_sb + ((size_t)(j / M) * M + j % M) * R;
-  } else if (j < 2 * S * M) {
-    const int jj = j - S * M;
-    src = rir_early ? rir_early + (size_t)b * early_sb + ((size_t)(jj / M) * M + jj % M) * R
-                    : rir_full + (size_t)b * full_sb + ((size_t)(jj / M) * M + jj % M) * R;
-  } else {
-    src = rir_full + (size_t)b * full_sb + ((size_t)S * M + (j - 2 * S * M)) * R;
-  }
-  const int r = rlen[b];
-  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < F; t += (long)gridDim.x * blockDim.x)
-    row[t] = t < r ? src[t] : 0.f;
-}
-
 int launched(const char* what) {
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -180,50 +117,6 @@ int launched(const char* what) {
 using namespace frir;
 
 extern "C" {
-
-int frir_mix_pack_dry(const float* dry, int64_t dry_stride_b, int64_t dry_stride_k, const float* noise,
-                      int64_t noise_stride, const int32_t* offsets, const int32_t* lengths,
-                      const int32_t* noise_len, const int32_t* dry_len, int32_t B, int32_t S, int64_t F,
-                      float* x, void* stream) {
-  if (!dry || !noise || !offsets || !lengths || !noise_len || !dry_len || !x || B < 0 || S < 1 || F < 1) {
-    set_error("frir_mix_pack_dry: invalid argument");
-    return FRIR_EINVAL;
-  }
-  if (B == 0) return FRIR_OK;
-  dim3 grid((unsigned)((F + 1023) / 1024 < 64 ? (F + 1023) / 1024 : 64), S + 1, B);
-  mix_pack_dry_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(dry, (long)dry_stride_b, (long)dry_stride_k, noise,
-                                                             (long)noise_stride, offsets, lengths, noise_len,
-                                                             dry_len, S, (long)F, x);
-  return launched("mix_pack_dry_kernel");
-}
-
-int frir_mix_pack_filters(const float* rir_full, int64_t full_stride_b, const float* rir_early,
-                          int64_t early_stride_b, const int32_t* rir_len, int32_t B, int32_t S, int32_t M,
-                          int64_t R, int64_t F, float* h, void* stream) {
-  if (!rir_full || !rir_len || !h || B < 0 || S < 1 || M < 1 || R < 1 || F < R) {
-    set_error("frir_mix_pack_filters: invalid argument");
-    return FRIR_EINVAL;
-  }
-  if (B == 0) return FRIR_OK;
-  dim3 grid((unsigned)((F + 1023) / 1024 < 64 ? (F + 1023) / 1024 : 64), (2 * S + 1) * M, B);
-  mix_pack_filters_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(rir_full, (long)full_stride_b, rir_early,
-                                                                 (long)early_stride_b, rir_len, S, M, (long)R,
-                                                                 (long)F, h);
-  return launched("mix_pack_filters_kernel");
-}
-
-int frir_mix_spectra(void* filt_spec, const void* dry_spec, const int32_t* src_of, int32_t B,
-                     int32_t J, int32_t K, int64_t Fc, void* stream) {
-  if (!filt_spec || !dry_spec || !src_of || B < 0 || J < 0 || K < 1 || Fc < 1) {
-    set_error("frir_mix_spectra: invalid argument");
-    return FRIR_EINVAL;
-  }
-  if (B == 0 || J == 0) return FRIR_OK;
-  dim3 grid((unsigned)std::min<long>((Fc + 1023) / 1024, 64), J, B);
-  mix_spectra_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((float2*)filt_spec, (const float2*)dry_spec,
-                                                            src_of, J, K, (long)Fc);
-  return launched("mix_spectra_kernel");
-}
 
 int frir_mix_powers(const float* y, int64_t F, const int64_t* req_row, const int32_t* req_lo,
                     const int32_t* req_hi, int32_t n_req, double* scratch, double* out, void* stream) {

@@ -6,12 +6,11 @@ mixture.py:225-332) and its ``MixtureSpec`` / ``MixtureResult`` types
 (:38-80, :107-113): same arguments, defaults, random draws (in the same order
 from the caller's ``numpy`` Generator), ``ValueError`` texts and metadata.
 
-The convolutions run batched on the device: one real FFT per dry signal
-(speakers placed at their offsets, the tiled point noise), one per filter row,
-then libfrir's kernels (``include/frir.h``: frir_mix_*) for the per-filter
-spectral products, the FP64 reference-channel powers, the SIR/SNR gains and
-the scaled references plus the mixture.  The FFTs themselves are cuFFT
-(through ``torch.fft``), the library call of this row.  ``mix_device`` is the
+The convolutions run batched on the device in libfrir's own partitioned
+overlap-save FFT convolution (``include/frir.h``: frir_mix_convolve, 8192-point
+shared-memory FFTs), then its kernels for the FP64 reference-channel powers,
+the SIR/SNR gains and the scaled references plus the mixture
+(frir_mix_powers / frir_mix_gains / frir_mix_combine).  ``mix_device`` is the
 batched tensor API (many utterances per launch); ``spatialize_and_mix`` is the
 drop-in for one utterance with numpy in and out.
 """
@@ -27,7 +26,7 @@ import numpy as np
 from . import _abi
 
 __all__ = ["MixtureSpec", "CurriculumState", "MixtureResult", "SyntheticPool", "curriculum_step",
-           "sample_scene", "scene_batch_jobs", "spatialize_and_mix", "mix_device", "generate_batch", "fft_size"]
+           "sample_scene", "scene_batch_jobs", "spatialize_and_mix", "mix_device", "generate_batch"]
 
 
 def _check_range(name, rng):
@@ -154,25 +153,6 @@ class MixtureResult:
     early_sources: list          # per speaker, (M, N) early-reverb reference
     noise: np.ndarray            # (M, N)
     metadata: dict
-
-
-def fft_size(n: int) -> int:
-    """Smallest 2^a 3^b 5^c (an efficient cuFFT length) holding a linear
-    convolution of length n: at most ~1.25 n instead of up to 2 n for a power
-    of two."""
-    n = max(1, int(n))
-    best = 1 << max(0, (n - 1).bit_length())
-    p5 = 1
-    while p5 < best:
-        p35 = p5
-        while p35 < best:
-            m = p35
-            while m < n:
-                m *= 2
-            best = min(best, m)
-            p35 *= 3
-        p5 *= 5
-    return best
 
 
 def _torch():

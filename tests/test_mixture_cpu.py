@@ -26,17 +26,25 @@ def test_spec_validation(kw, msg):
         MX.MixtureSpec(**kw)
 
 
-def test_fft_size():
-    assert MX.fft_size(1) == 1 and MX.fft_size(2) == 2 and MX.fft_size(3) == 3 and MX.fft_size(7) == 8
-    assert MX.fft_size(65536) == 65536 and MX.fft_size(70399) == 72000
-    for n in (1, 17, 1000, 70399, 131073, 999999):
-        m = MX.fft_size(n)
-        assert m >= n and m < 1.25 * n + 8
-        r = m
-        for p in (2, 3, 5):
-            while r % p == 0:
-                r //= p
-        assert r == 1
+def test_convolve_scratch_sizes():
+    """frir_mix_convolve_scratch (host-side sizing, no GPU): spectra of every
+    4096-sample block of each source plus every filter partition of each row
+    pair, 8192 complex64 bins each; y rows padded to whole blocks."""
+    import ctypes
+
+    from paper_2304_08052_b200 import _abi
+
+    lib = _abi.lib()
+    ys = ctypes.c_int64(0)
+    B, S, M, R, T = 3, 2, 4, 9000, 70000
+    got = lib.frir_mix_convolve_scratch(B, S, M, R, T, ctypes.byref(ys))
+    nb, q, pairs = -(-T // 4096), -(-R // 4096), S * M + (M + 1) // 2
+    assert ys.value == nb * 4096
+    assert got == (B * (S + 1) * nb + B * pairs * q) * 8192 * 8
+    lib.frir_mix_convolve_scratch(1, 1, 3, 1, 1, ctypes.byref(ys))
+    assert ys.value == 4096
+    assert lib.frir_mix_convolve_scratch(1, 0, 4, 10, 10, None) == -1
+    assert lib.frir_mix_convolve_scratch(1, 1, 4, 0, 10, None) == -1
 
 
 @pytest.mark.parametrize("ci", [4, 5])
