@@ -74,8 +74,10 @@ __global__ void mix_gains_kernel(const double* __restrict__ pw, const double* __
 // Scaled outputs and the mixture (mixture.py:293-313):
 //   sources[b][k][m][t] = g_k y[b][kM + m][t], early[b][k][m][t] = g_k y[b][(S + k)M + m][t],
 //   noise[b][m][t] = g_n y[b][2SM + m][t], mixture = sum_k sources + noise,
-// for t < total_b (zeros up to T).  Grid (t blocks, M, B).
-__global__ void mix_combine_kernel(const float* __restrict__ y, const double* __restrict__ gains,
+// for t < total_b (zeros up to T).  Grid (T / (256 kCombineU), M, B): each
+// thread takes kCombineU samples 256 apart, all loads issued before the stores.
+constexpr int kCombineU = 4;
+__global__ void __launch_bounds__(256) mix_combine_kernel(const float* __restrict__ y, const double* __restrict__ gains,
                                    const int32_t* __restrict__ total, int S, int M, long F, long T,
                                    float* __restrict__ mixture, float* __restrict__ sources,
                                    float* __restrict__ early, float* __restrict__ noise) {
@@ -83,22 +85,54 @@ __global__ void mix_combine_kernel(const float* __restrict__ y, const double* __
   const int J = (2 * S + 1) * M;
   const float* yb = y + (size_t)b * J * F;
   const double* g = gains + (size_t)b * (S + 1);
-  const int tot = total[b];
+  const long tot = total[b];
+  const long t0 = (long)blockIdx.x * (256 * kCombineU) + threadIdx.x;
+  float mix[kCombineU], nv[kCombineU], v[kCombineU];
   const float gn = (float)g[S];
-  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < T; t += (long)gridDim.x * blockDim.x) {
-    const bool in = t < tot;
-    float mix = 0.f;
-    for (int k = 0; k < S; ++k) {
-      const float gk = (float)g[k];
-      const float vf = in ? gk * yb[(size_t)(k * M + m) * F + t] : 0.f;
-      const float ve = in ? gk * yb[(size_t)((S + k) * M + m) * F + t] : 0.f;
-      sources[(((size_t)b * S + k) * M + m) * T + t] = vf;
-      early[(((size_t)b * S + k) * M + m) * T + t] = ve;
-      mix += vf;
+  const float* yn = yb + (size_t)(2 * S * M + m) * F;
+#pragma unroll
+  for (int i = 0; i < kCombineU; ++i) {
+    const long t = t0 + i * 256;
+    nv[i] = t < tot ? gn * yn[t] : 0.f;
+    mix[i] = 0.f;
+  }
+#pragma unroll
+  for (int i = 0; i < kCombineU; ++i) {
+    const long t = t0 + i * 256;
+    if (t < T) noise[((size_t)b * M + m) * T + t] = nv[i];
+  }
+  for (int k = 0; k < S; ++k) {
+    const float gk = (float)g[k];
+    const float* yf = yb + (size_t)(k * M + m) * F;
+    const float* ye = yb + (size_t)((S + k) * M + m) * F;
+    float* so = sources + (((size_t)b * S + k) * M + m) * T;
+    float* eo = early + (((size_t)b * S + k) * M + m) * T;
+#pragma unroll
+    for (int i = 0; i < kCombineU; ++i) {
+      const long t = t0 + i * 256;
+      v[i] = t < tot ? gk * yf[t] : 0.f;
     }
-    const float vn = in ? gn * yb[(size_t)(2 * S * M + m) * F + t] : 0.f;
-    noise[((size_t)b * M + m) * T + t] = vn;
-    mixture[((size_t)b * M + m) * T + t] = mix + vn;
+#pragma unroll
+    for (int i = 0; i < kCombineU; ++i) {
+      const long t = t0 + i * 256;
+      if (t < T) so[t] = v[i];
+      mix[i] += v[i];
+    }
+#pragma unroll
+    for (int i = 0; i < kCombineU; ++i) {
+      const long t = t0 + i * 256;
+      v[i] = t < tot ? gk * ye[t] : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < kCombineU; ++i) {
+      const long t = t0 + i * 256;
+      if (t < T) eo[t] = v[i];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kCombineU; ++i) {
+    const long t = t0 + i * 256;
+    if (t < T) mixture[((size_t)b * M + m) * T + t] = mix[i] + nv[i];  // sum of the sources, then the noise
   }
 }
 
@@ -152,7 +186,7 @@ int frir_mix_combine(const float* y, const double* gains, const int32_t* total, 
     return FRIR_EINVAL;
   }
   if (B == 0 || T == 0) return FRIR_OK;
-  dim3 grid((unsigned)std::min<long>((T + 1023) / 1024, 64), M, B);
+  dim3 grid((unsigned)((T + 256 * kCombineU - 1) / (256 * kCombineU)), M, B);
   mix_combine_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(y, gains, total, S, M, (long)F, (long)T,
                                                             mixture, sources, early, noise);
   return launched("mix_combine_kernel");
