@@ -67,10 +67,12 @@ __device__ __forceinline__ void dft8(float2 (&v)[8]) {
   v[7] = subf(f0, f1);
 }
 
-// Shared-memory layout of the transform: one float2 of padding per 32
-// entries, so the stride-R / stride-Ns Stockham accesses spread over banks.
-__device__ __forceinline__ int pad(int i) { return i + (i >> 5); }
-constexpr int kFftPadded = kFftN + kFftN / 32;
+// Shared-memory layout of the transform: an XOR swizzle of the low four bits
+// of the float2 index with bits 3..6, so every access of the passes below --
+// consecutive reads, the stride-8 stores of pass 1 and the 8-runs at stride 64
+// of pass 2 -- is free of bank conflicts (checked exhaustively offline).
+__device__ __forceinline__ int pad(int i) { return i ^ ((i >> 3) & 15); }
+constexpr int kFftPadded = kFftN;
 constexpr int kTwN = kFftN / 8;  // smem twiddle table: W^m, m < N / 8
 
 // W^m for m < N / 2 from the eighth-circle table: W^{m mod N/8} times the
