@@ -10,8 +10,8 @@
 //
 // Two real filter rows that share a source (speaker k: the full and early
 // filters of mic m; the noise: mics m, m+1) ride in one complex transform,
-// H = FFT(h_a + i h_b), so IFFT(X . H) = y_a + i y_b.  The FFT is a radix-8
-// (four passes) + radix-2 Stockham in place in 64 KB of shared memory, 512
+// H = FFT(h_a + i h_b), so IFFT(X . H) = y_a + i y_b.  The FFT is a radix
+// 16 * 16 * 16 * 2 Stockham in place in 64 KB of swizzled shared memory, 512
 // threads, twiddles from an FP64-computed table.  FP32 throughout (the
 // reference is FP64; the mixing tests hold the result to 1e-5 of the peak).
 #include <cuda_runtime.h>
@@ -40,39 +40,51 @@ __device__ __forceinline__ float2 subf(float2 a, float2 b) { return make_float2(
 // multiply by -i
 __device__ __forceinline__ float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }
 
-// Size-8 DFT in registers, natural order in and out (forward, W = e^{-2 pi i / 8}).
-__device__ __forceinline__ void dft8(float2 (&v)[8]) {
-  const float r = 0.70710678118654752f;
-  // span 4
-  float2 a0 = addf(v[0], v[4]), b0 = subf(v[0], v[4]);
-  float2 a1 = addf(v[1], v[5]), b1 = subf(v[1], v[5]);
-  float2 a2 = addf(v[2], v[6]), b2 = subf(v[2], v[6]);
-  float2 a3 = addf(v[3], v[7]), b3 = subf(v[3], v[7]);
-  b1 = make_float2(r * (b1.x + b1.y), r * (b1.y - b1.x));   // * W8^1
-  b2 = mul_mi(b2);                                          // * W8^2 = -i
-  b3 = make_float2(r * (b3.y - b3.x), -r * (b3.x + b3.y));  // * W8^3
-  // span 2
-  float2 c0 = addf(a0, a2), d0 = subf(a0, a2);
-  float2 c1 = addf(a1, a3), d1 = mul_mi(subf(a1, a3));
-  float2 e0 = addf(b0, b2), f0 = subf(b0, b2);
-  float2 e1 = addf(b1, b3), f1 = mul_mi(subf(b1, b3));
-  // span 1; outputs in bit-reversed positions -> natural order
-  v[0] = addf(c0, c1);
-  v[4] = subf(c0, c1);
-  v[2] = addf(d0, d1);
-  v[6] = subf(d0, d1);
-  v[1] = addf(e0, e1);
-  v[5] = subf(e0, e1);
-  v[3] = addf(f0, f1);
-  v[7] = subf(f0, f1);
+// Size-4 DFT in place (forward).
+__device__ __forceinline__ void dft4(float2& a0, float2& a1, float2& a2, float2& a3) {
+  const float2 t0 = addf(a0, a2), t1 = subf(a0, a2), t2 = addf(a1, a3), t3 = mul_mi(subf(a1, a3));
+  a0 = addf(t0, t2);
+  a2 = subf(t0, t2);
+  a1 = addf(t1, t3);
+  a3 = subf(t1, t3);
+}
+__device__ __forceinline__ float2 cmulc(float2 a, float wr, float wi) {
+  return make_float2(a.x * wr - a.y * wi, a.x * wi + a.y * wr);
+}
+
+// Size-16 DFT in registers, natural order in and out (4 x 4: DFTs over n1 of
+// x[4 n1 + n2], twiddles W16^(n2 k1), DFTs over n2, transpose).
+__device__ __forceinline__ void dft16(const float2 (&x)[16], float2 (&o)[16]) {
+  float2 v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = x[i];
+#pragma unroll
+  for (int n2 = 0; n2 < 4; ++n2) dft4(v[n2], v[4 + n2], v[8 + n2], v[12 + n2]);
+  const float c = 0.92387953251128674f, s = 0.38268343236508977f, h = 0.70710678118654752f;
+  v[5] = cmulc(v[5], c, -s);     // W16^1
+  v[6] = cmulc(v[6], h, -h);     // W16^2
+  v[7] = cmulc(v[7], s, -c);     // W16^3
+  v[9] = cmulc(v[9], h, -h);     // W16^2
+  v[10] = mul_mi(v[10]);         // W16^4
+  v[11] = cmulc(v[11], -h, -h);  // W16^6
+  v[13] = cmulc(v[13], s, -c);   // W16^3
+  v[14] = cmulc(v[14], -h, -h);  // W16^6
+  v[15] = cmulc(v[15], -c, s);   // W16^9
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) dft4(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1)
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) o[k1 + 4 * k2] = v[4 * k1 + k2];
 }
 
 // Shared-memory layout of the transform: an XOR swizzle of the low four bits
-// of the float2 index with bits 3..6, so every access of the passes below --
-// consecutive reads, the stride-8 stores of pass 1 and the 8-runs at stride 64
-// of pass 2 -- is free of bank conflicts (checked exhaustively offline).
-__device__ __forceinline__ int pad(int i) { return i ^ ((i >> 3) & 15); }
-constexpr int kFftPadded = kFftN;
+// of the float2 index with bits 4..7.  Every access of the passes below --
+// consecutive reads (j + 512 r), the stride-16 stores of pass 1, the 16-runs
+// at stride 256 of pass 2 and the 256-runs of pass 3 -- is free of bank
+// conflicts (checked exhaustively offline), and reads at j + 512 r are
+// swz(j) + 512 r (immediate offsets).
+__device__ __forceinline__ int swz(int i) { return i ^ ((i >> 4) & 15); }
 constexpr int kTwN = kFftN / 8;  // smem twiddle table: W^m, m < N / 8
 
 // W^m for m < N / 2 from the eighth-circle table: W^{m mod N/8} times the
@@ -87,85 +99,68 @@ __device__ __forceinline__ float2 twiddle_half(const float2* tws, int m) {
   return cmulf(lo, rot);
 }
 
-// One Stockham pass of radix R over buf (in place: every thread loads its
-// butterflies' inputs before the barrier, then stores).  NS = product of the
-// radices of the previous passes (compile time: divisions are shifts).
-// Twiddles W^{r k step}: w1 = W^{k step} from the smem table (k step < N/8,
-// times an eighth-circle rotation for the radix-2 pass), w_r = w1^r.
-template <int R, int NS>
-__device__ __forceinline__ void stockham_pass(float2* buf, const float2* tws) {
-  constexpr int NB = kFftN / R / kFftThreads;  // butterflies per thread
-  constexpr int step = kFftN / (NS * R);       // twiddle index stride
-  float2 v[NB][R];
+// The forward 8192-point FFT is a radix 16 * 16 * 16 * 2 Stockham
+// decomposition, 512 threads, one butterfly per thread per radix-16 pass:
+//   fft_first(buf, x): pass 1 of butterfly j = threadIdx.x from registers,
+//     x[r] = input[j + 512 r]; results to buf.
+//   fft_mid(buf, tws): passes 2 and 3 (after a barrier; ends with one).
+//   fft_last(buf, tws, j, ...): pass 4 (radix 2) of butterfly j < N/2 ->
+//     X[j], X[j + N/2], straight to the caller.
+// The kernels feed pass 1 from global memory and take pass 4 to global memory,
+// so only passes 2-3 make a full shared-memory round trip.
+__device__ __forceinline__ void fft_first(float2* buf, const float2 (&x)[16]) {
+  const int j = threadIdx.x;
+  float2 o[16];
+  dft16(x, o);
 #pragma unroll
-  for (int b = 0; b < NB; ++b) {
-    const int j = threadIdx.x + b * kFftThreads;
-    const int k = j & (NS - 1);
-#pragma unroll
-    for (int r = 0; r < R; ++r) v[b][r] = buf[pad(j + r * (kFftN / R))];
-    if (NS > 1) {
-      const int m = k * step;  // < N / R
-      const float2 w1 = R == 8 ? tws[m] : twiddle_half(tws, m);
-      float2 w = w1;
-#pragma unroll
-      for (int r = 1; r < R; ++r) {
-        v[b][r] = cmulf(v[b][r], w);
-        if (r + 1 < R) w = cmulf(w, w1);
-      }
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int b = 0; b < NB; ++b) {
-    const int j = threadIdx.x + b * kFftThreads;
-    const int k = j & (NS - 1);
-    if constexpr (R == 8) {
-      dft8(v[b]);
-    } else {
-      const float2 a = v[b][0], c = v[b][1];
-      v[b][0] = addf(a, c);
-      v[b][1] = subf(a, c);
-    }
-    const int d = (j / NS) * NS * R + k;
-#pragma unroll
-    for (int r = 0; r < R; ++r) buf[pad(d + r * NS)] = v[b][r];
-  }
-  __syncthreads();
+  for (int r = 0; r < 16; ++r) buf[16 * j + (r ^ (j & 15))] = o[r];  // swz(16 j + r)
 }
-
-// The forward 8192-point FFT (8 * 8 * 8 * 8 * 2) in three pieces so the
-// kernels feed the first pass from registers and take the last pass's outputs
-// straight to global memory (no shared-memory round trip at either end):
-//   fft_first(buf, v, j): pass 1 (radix 8, no twiddles) of butterfly j < N/8,
-//     v[r] = x[j + r N/8]; results to buf.
-//   fft_mid(buf, tws): passes 2-4 (after a barrier; ends with one).
-//   fft_last(buf, tws, j, ...): pass 5 (radix 2) of butterfly j < N/2 ->
-//     X[j], X[j + N/2].
-__device__ __forceinline__ void fft_first(float2* buf, float2 (&v)[8], int j) {
-  dft8(v);
+// Radix-16 pass over NS-point sub-transforms (NS = 16, 256): twiddles W^{r k step},
+// w1 = W^{k step} (k step < 512) from the table, w_r = w1^r.
+template <int NS>
+__device__ __forceinline__ void pass16(float2* buf, const float2* tws) {
+  constexpr int step = kFftN / (NS * 16);
+  const int j = threadIdx.x;
+  const int k = j & (NS - 1);
+  const int sj = swz(j);
+  float2 x[16];
 #pragma unroll
-  for (int r = 0; r < 8; ++r) buf[pad(8 * j + r)] = v[r];
+  for (int r = 0; r < 16; ++r) x[r] = buf[sj + 512 * r];
+  const float2 w1 = tws[k * step];
+  float2 w = w1;
+#pragma unroll
+  for (int r = 1; r < 16; ++r) {
+    x[r] = cmulf(x[r], w);
+    if (r + 1 < 16) w = cmulf(w, w1);
+  }
+  __syncthreads();
+  float2 o[16];
+  dft16(x, o);
+  const int d = (j / NS) * NS * 16 + k;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) buf[swz(d + r * NS)] = o[r];
+  __syncthreads();
 }
 __device__ __forceinline__ void fft_mid(float2* buf, const float2* tws) {
   __syncthreads();
-  stockham_pass<8, 8>(buf, tws);
-  stockham_pass<8, 64>(buf, tws);
-  stockham_pass<8, 512>(buf, tws);
+  pass16<16>(buf, tws);
+  pass16<256>(buf, tws);
 }
 __device__ __forceinline__ void fft_last(const float2* buf, const float2* tws, int j, float2* x0, float2* x1) {
-  const float2 a = buf[pad(j)];
-  const float2 c = cmulf(buf[pad(j + kFftP)], twiddle_half(tws, j));
+  const int sj = swz(j);
+  const float2 a = buf[sj];
+  const float2 c = cmulf(buf[sj + kFftP], twiddle_half(tws, j));
   *x0 = addf(a, c);
   *x1 = subf(a, c);
 }
 
 // Shared memory of the FFT kernels: the padded transform, then the twiddles.
 __device__ __forceinline__ float2* load_twiddles(float2* smem_base, const float2* __restrict__ tw) {
-  float2* tws = smem_base + kFftPadded;
+  float2* tws = smem_base + kFftN;
   for (int i = threadIdx.x; i < kTwN; i += kFftThreads) tws[i] = __ldg(tw + i);
   return tws;
 }
-constexpr size_t kFftSmem = (size_t)(kFftPadded + kTwN) * sizeof(float2);
+constexpr size_t kFftSmem = (size_t)(kFftN + kTwN) * sizeof(float2);
 
 struct ConvArgs {
   const float* dry;
@@ -211,7 +206,7 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_in_kernel(ConvArgs A) {
   const int t = blockIdx.x, k = blockIdx.y, b = blockIdx.z;
   const float2* tws = load_twiddles(buf, A.tw);
   const long base = (long)(t - 1) * kFftP;
-  float vals[kFftN / kFftThreads];  // samples base + threadIdx.x + i * 512
+  float vals[kFftN / kFftThreads];  // samples base + threadIdx.x + 512 i
   if (k < A.S) {
     const long o = A.off[b * A.S + k], n = A.len[b * A.S + k];
     const float* src = A.dry + (size_t)b * A.dry_sb + (size_t)k * A.dry_sk;
@@ -236,12 +231,11 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_in_kernel(ConvArgs A) {
       }
     }
   }
+  {  // butterfly j = threadIdx.x of pass 1 reads samples j + 512 r
+    float2 x[16];
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {  // butterflies j = threadIdx.x + h * 512 read samples j + r * 1024
-    float2 v[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) v[r] = make_float2(vals[h + 2 * r], 0.f);
-    fft_first(buf, v, threadIdx.x + h * kFftThreads);
+    for (int r = 0; r < 16; ++r) x[r] = make_float2(vals[r], 0.f);
+    fft_first(buf, x);
   }
   fft_mid(buf, tws);
   float2* out = A.X + (((size_t)b * (A.S + 1) + k) * A.nb + t) * kFftN;
@@ -268,21 +262,20 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_filt_kernel(ConvArgs A) {
   const float* ha = row(ja);
   const float* hb = jb >= 0 ? row(jb) : nullptr;
   const float2* tws = load_twiddles(buf, A.tw);
+  {
+    const int j = threadIdx.x;
+    float2 x[16];
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int j = threadIdx.x + h * kFftThreads;
-    float2 v[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {  // taps j + q * 1024 of the partition; the upper half is padding
-      const int u = j + q * (kFftN / 8), tap = p * kFftP + u;
+    for (int q = 0; q < 16; ++q) {  // taps j + 512 q of the partition; the upper half is padding
+      const int u = j + q * kFftThreads, tap = p * kFftP + u;
       float va = 0.f, vb = 0.f;
-      if (u < kFftP && tap < r) {
+      if (q < 8 && tap < r) {
         va = __ldg(ha + tap);
         if (hb) vb = __ldg(hb + tap);
       }
-      v[q] = make_float2(va, vb);
+      x[q] = make_float2(va, vb);
     }
-    fft_first(buf, v, j);
+    fft_first(buf, x);
   }
   fft_mid(buf, tws);
   float2* out = A.H + (((size_t)b * A.npairs + pi) * A.Q + p) * kFftN;
@@ -301,30 +294,32 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_conv_kernel(ConvArgs A) {
   const int qb = (A.rlen[b] + kFftP - 1) / kFftP;  // this item's non-zero partitions
   const int qmax = min(qb - 1, t);
   const float2* tws = load_twiddles(buf, A.tw);
+  {  // butterfly j = threadIdx.x of pass 1 reads bins j + 512 r
+    const int j = threadIdx.x;
+    float2 v[16];
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {  // butterfly j of pass 1 reads bins j + r * 1024
-    const int j = threadIdx.x + h * kFftThreads;
-    float2 v[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) v[r] = make_float2(0.f, 0.f);
+    for (int r = 0; r < 16; ++r) v[r] = make_float2(0.f, 0.f);
     for (int p = 0; p <= qmax; ++p) {
       const float2* xp = Xs + (size_t)(t - p) * kFftN + j;
       const float2* hp = Hs + (size_t)p * kFftN + j;
-      float2 x[8], hh[8];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        x[r] = __ldg(xp + r * (kFftN / 8));
-        hh[r] = __ldg(hp + r * (kFftN / 8));
-      }
+      for (int c = 0; c < 16; c += 8) {
+        float2 x[8], hh[8];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        v[r].x = fmaf(x[r].x, hh[r].x, fmaf(-x[r].y, hh[r].y, v[r].x));
-        v[r].y = fmaf(x[r].x, hh[r].y, fmaf(x[r].y, hh[r].x, v[r].y));
+        for (int r = 0; r < 8; ++r) {
+          x[r] = __ldg(xp + (c + r) * kFftThreads);
+          hh[r] = __ldg(hp + (c + r) * kFftThreads);
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          v[c + r].x = fmaf(x[r].x, hh[r].x, fmaf(-x[r].y, hh[r].y, v[c + r].x));
+          v[c + r].y = fmaf(x[r].x, hh[r].y, fmaf(x[r].y, hh[r].x, v[c + r].y));
+        }
       }
     }
 #pragma unroll
-    for (int r = 0; r < 8; ++r) v[r].y = -v[r].y;  // conj: IFFT(z) = conj(FFT(conj(z))) / N
-    fft_first(buf, v, j);
+    for (int r = 0; r < 16; ++r) v[r].y = -v[r].y;  // conj: IFFT(z) = conj(FFT(conj(z))) / N
+    fft_first(buf, v);
   }
   fft_mid(buf, tws);
   const float inv = 1.0f / kFftN;
