@@ -32,8 +32,9 @@ constexpr int kFftN = 8192;            // transform length
 constexpr int kFftP = kFftN / 2;       // hop / partition length
 constexpr int kFftThreads = 512;
 
+// (the library builds with -fmad=false for the FP64 geometry; the FFTs fuse explicitly)
 __device__ __forceinline__ float2 cmulf(float2 a, float2 b) {
-  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
 __device__ __forceinline__ float2 addf(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 subf(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
@@ -49,7 +50,7 @@ __device__ __forceinline__ void dft4(float2& a0, float2& a1, float2& a2, float2&
   a3 = subf(t1, t3);
 }
 __device__ __forceinline__ float2 cmulc(float2 a, float wr, float wi) {
-  return make_float2(a.x * wr - a.y * wi, a.x * wi + a.y * wr);
+  return make_float2(fmaf(a.x, wr, -a.y * wi), fmaf(a.x, wi, a.y * wr));
 }
 
 // Size-16 DFT in registers, natural order in and out (4 x 4: DFTs over n1 of
@@ -104,8 +105,8 @@ __device__ __forceinline__ float2 twiddle_half(const float2* tws, int m) {
 //   fft_first(buf, x): pass 1 of butterfly j = threadIdx.x from registers,
 //     x[r] = input[j + 512 r]; results to buf.
 //   fft_mid(buf, tws): passes 2 and 3 (after a barrier; ends with one).
-//   fft_last(buf, tws, j, ...): pass 4 (radix 2) of butterfly j < N/2 ->
-//     X[j], X[j + N/2], straight to the caller.
+//   fft_last(buf, tws, f): pass 4 (radix 2), f(j, X[j], X[j + N/2]) for the
+//     thread's eight butterflies j < N/2, straight to the caller.
 // The kernels feed pass 1 from global memory and take pass 4 to global memory,
 // so only passes 2-3 make a full shared-memory round trip.
 __device__ __forceinline__ void fft_first(float2* buf, const float2 (&x)[16]) {
@@ -146,12 +147,25 @@ __device__ __forceinline__ void fft_mid(float2* buf, const float2* tws) {
   pass16<16>(buf, tws);
   pass16<256>(buf, tws);
 }
-__device__ __forceinline__ void fft_last(const float2* buf, const float2* tws, int j, float2* x0, float2* x1) {
-  const int sj = swz(j);
-  const float2 a = buf[sj];
-  const float2 c = cmulf(buf[sj + kFftP], twiddle_half(tws, j));
-  *x0 = addf(a, c);
-  *x1 = subf(a, c);
+// Pass 4 for the butterflies j = threadIdx.x + 512 b, b < 8: f(j, X[j], X[j + N/2]).
+// W^j = W^t * W^{512 b}: one table read per thread, the eight W^{512 b} are
+// constants.
+template <typename F>
+__device__ __forceinline__ void fft_last(const float2* buf, const float2* tws, F&& f) {
+  constexpr float kC[8] = {1.f, 0.92387953251128674f, 0.70710678118654752f, 0.38268343236508977f,
+                           0.f, -0.38268343236508977f, -0.70710678118654752f, -0.92387953251128674f};
+  constexpr float kS[8] = {0.f, 0.38268343236508977f, 0.70710678118654752f, 0.92387953251128674f,
+                           1.f, 0.92387953251128674f, 0.70710678118654752f, 0.38268343236508977f};
+  const int t = threadIdx.x;
+  const float2 wt = tws[t];
+  const int st = swz(t);  // swz(t + 512 b) = swz(t) + 512 b
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const float2 w = b == 0 ? wt : cmulc(wt, kC[b], -kS[b]);
+    const float2 a = buf[st + 512 * b];
+    const float2 c = cmulf(buf[st + 512 * b + kFftP], w);
+    f(t + 512 * b, addf(a, c), subf(a, c));
+  }
 }
 
 // Shared memory of the FFT kernels: the padded transform, then the twiddles.
@@ -239,7 +253,10 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_in_kernel(ConvArgs A) {
   }
   fft_mid(buf, tws);
   float2* out = A.X + (((size_t)b * (A.S + 1) + k) * A.nb + t) * kFftN;
-  for (int j = threadIdx.x; j < kFftP; j += kFftThreads) fft_last(buf, tws, j, out + j, out + j + kFftP);
+  fft_last(buf, tws, [&](int j, float2 x0, float2 x1) {
+    out[j] = x0;
+    out[j + kFftP] = x1;
+  });
 }
 
 // H_p = FFT(h_a + i h_b) over taps [pP, pP + P).  Grid (Q, npairs, B).
@@ -279,7 +296,10 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_filt_kernel(ConvArgs A) {
   }
   fft_mid(buf, tws);
   float2* out = A.H + (((size_t)b * A.npairs + pi) * A.Q + p) * kFftN;
-  for (int j = threadIdx.x; j < kFftP; j += kFftThreads) fft_last(buf, tws, j, out + j, out + j + kFftP);
+  fft_last(buf, tws, [&](int j, float2 x0, float2 x1) {
+    out[j] = x0;
+    out[j + kFftP] = x1;
+  });
 }
 
 // Output block t of a pair: sum_p X_{t-p} H_p, inverse FFT (conj trick),
@@ -325,12 +345,10 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_conv_kernel(ConvArgs A) {
   const float inv = 1.0f / kFftN;
   float* ya = A.y + ((size_t)b * ((2 * A.S + 1) * A.M) + ja) * A.y_stride + (size_t)t * kFftP;
   float* yb = jb >= 0 ? A.y + ((size_t)b * ((2 * A.S + 1) * A.M) + jb) * A.y_stride + (size_t)t * kFftP : nullptr;
-  for (int n = threadIdx.x; n < kFftP; n += kFftThreads) {  // the last P outputs: X[n + P]
-    float2 z0, z1;
-    fft_last(buf, tws, n, &z0, &z1);
+  fft_last(buf, tws, [&](int n, float2, float2 z1) {  // the last P outputs: X[n + P]
     ya[n] = z1.x * inv;
     if (yb) yb[n] = -z1.y * inv;
-  }
+  });
 }
 
 // Twiddle table exp(-2 pi i m / N), m < N, per device (FP64-computed).
