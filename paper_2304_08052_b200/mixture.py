@@ -161,6 +161,25 @@ def _torch():
     return torch
 
 
+def _upload(dev, parts):
+    """Device copies of small host arrays through one pinned staging block and
+    one non-blocking copy on the current stream; returns views of one device
+    buffer in the order given (int32 / int64 / float64)."""
+    torch = _torch()
+    dt = {np.dtype(np.int32): torch.int32, np.dtype(np.int64): torch.int64, np.dtype(np.float64): torch.float64}
+    offs, n = [], 0
+    for a in parts:
+        n = (n + 7) & ~7
+        offs.append(n)
+        n += a.nbytes
+    host = torch.empty(max(n, 8), dtype=torch.uint8, pin_memory=True)
+    hv = host.numpy()
+    for a, o in zip(parts, offs):
+        hv[o:o + a.nbytes] = np.ascontiguousarray(a).view(np.uint8).ravel()
+    buf = host.to(dev, non_blocking=True)  # the caching host allocator keeps `host` until the copy is done
+    return [buf[o:o + a.nbytes].view(dt[a.dtype]) for a, o in zip(parts, offs)]
+
+
 def mix_device(dry, dry_len, offsets, noise, noise_len, rir_full, rir_early, rir_len, sir_db, snr_db,
                sir_scope: str = "full"):
     """Batched spatialise-and-mix of B utterances on one device.
@@ -190,8 +209,6 @@ def mix_device(dry, dry_len, offsets, noise, noise_len, rir_full, rir_early, rir
     T = int(total.max()) if B else 0
     lib = _abi.lib()
     stream = torch.cuda.current_stream(dev).cuda_stream
-
-    i32 = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32), device=dev)  # noqa: E731
     dry = dry.contiguous()
     noise = noise.contiguous()
     # filters: each item's [S(+1)][M][R] block must be contiguous; items may be strided
@@ -202,25 +219,8 @@ def mix_device(dry, dry_len, offsets, noise, noise_len, rir_full, rir_early, rir
         raise ValueError("rir_early must be (B, >= S, M, R) like rir_full")
     if rir_early is not None and rir_early.stride()[1:] != (M * R, R, 1):
         rir_early = rir_early.contiguous()
-    # convolution of every filter row with its source: libfrir's hand-written
-    # partitioned overlap-save FFT convolution (placed speakers, tiled noise)
-    dlen = total - rir_len + 1
-    off_d, len_d, nlen_d, dlen_d = i32(offsets), i32(dry_len), i32(noise_len), i32(dlen)
-    rl = i32(rir_len)
     J = (2 * S + 1) * M
-    ys = ctypes.c_int64(0)
-    nscr = lib.frir_mix_convolve_scratch(B, S, M, R, T, ctypes.byref(ys))
-    F = int(ys.value)  # row stride of y
-    scratch = torch.empty(max(int(nscr), 1), dtype=torch.uint8, device=dev)
-    y = torch.empty((B, J, F), dtype=torch.float32, device=dev)
-    _abi.check(lib.frir_mix_convolve(
-        dry.data_ptr(), dry.stride(0), dry.stride(1), noise.data_ptr(), noise.stride(0), off_d.data_ptr(),
-        len_d.data_ptr(), nlen_d.data_ptr(), dlen_d.data_ptr(), rir_full.data_ptr(), rir_full.stride(0),
-        rir_early.data_ptr() if rir_early is not None else None, rir_early.stride(0) if rir_early is not None else 0,
-        rl.data_ptr(), B, S, M, R, T, scratch.data_ptr(), scratch.numel(), y.data_ptr(), F, stream),
-        "frir_mix_convolve")
-    del scratch
-
+    dlen = total - rir_len + 1
     # reference-channel power requests (mixture.py:284-303, 311), per item:
     # p_ref, (p_int_k, p_tgt_k) for k = 1..S-1, p_noise
     base = np.arange(B, dtype=np.int64) * J
@@ -238,20 +238,35 @@ def mix_device(dry, dry_len, offsets, noise, noise_len, rir_full, rir_early, rir
             lo[:, 2 * k - 1] = lo[:, 2 * k] = a
             hi[:, 2 * k - 1] = hi[:, 2 * k] = e
     rows, lo, hi = rows.ravel(), lo.ravel(), hi.ravel()
-    req_row = torch.as_tensor(rows, device=dev)
-    req_lo = i32(lo)
-    req_hi = i32(hi)
+    i32 = lambda a: np.asarray(a, dtype=np.int32).ravel()  # noqa: E731
+    # every small per-item table in one pinned block and one async copy (no
+    # pageable copies that would stall the host behind the queued kernels)
+    (off_d, len_d, nlen_d, dlen_d, rl, req_row, req_lo, req_hi, tot_d, sir, snr) = _upload(dev, [
+        i32(offsets), i32(dry_len), i32(noise_len), i32(dlen), i32(rir_len), rows, i32(lo), i32(hi), i32(total),
+        np.asarray(sir_db, dtype=np.float64).reshape(B * max(S - 1, 1)),
+        np.asarray(snr_db, dtype=np.float64).reshape(B)])
+    # convolution of every filter row with its source: libfrir's hand-written
+    # partitioned overlap-save FFT convolution (placed speakers, tiled noise)
+    ys = ctypes.c_int64(0)
+    nscr = lib.frir_mix_convolve_scratch(B, S, M, R, T, ctypes.byref(ys))
+    F = int(ys.value)  # row stride of y
+    scratch = torch.empty(max(int(nscr), 1), dtype=torch.uint8, device=dev)
+    y = torch.empty((B, J, F), dtype=torch.float32, device=dev)
+    _abi.check(lib.frir_mix_convolve(
+        dry.data_ptr(), dry.stride(0), dry.stride(1), noise.data_ptr(), noise.stride(0), off_d.data_ptr(),
+        len_d.data_ptr(), nlen_d.data_ptr(), dlen_d.data_ptr(), rir_full.data_ptr(), rir_full.stride(0),
+        rir_early.data_ptr() if rir_early is not None else None, rir_early.stride(0) if rir_early is not None else 0,
+        rl.data_ptr(), B, S, M, R, T, scratch.data_ptr(), scratch.numel(), y.data_ptr(), F, stream),
+        "frir_mix_convolve")
+    del scratch
     pw = torch.empty(len(rows), dtype=torch.float64, device=dev)
     scratch = torch.empty(len(rows) * _abi.MIX_POWER_CHUNKS, dtype=torch.float64, device=dev)
     _abi.check(lib.frir_mix_powers(y.data_ptr(), F, req_row.data_ptr(), req_lo.data_ptr(),
                                    req_hi.data_ptr(), len(rows), scratch.data_ptr(), pw.data_ptr(), stream),
                "frir_mix_powers")
-    sir = torch.as_tensor(np.asarray(sir_db, dtype=np.float64).reshape(B, max(S - 1, 1)), device=dev)
-    snr = torch.as_tensor(np.asarray(snr_db, dtype=np.float64).reshape(B), device=dev)
     gains = torch.empty((B, S + 1), dtype=torch.float64, device=dev)
     _abi.check(lib.frir_mix_gains(pw.data_ptr(), sir.data_ptr(), snr.data_ptr(), B, S, gains.data_ptr(),
                                   stream), "frir_mix_gains")
-    tot_d = torch.as_tensor(total.astype(np.int32), device=dev)
     out = {
         "mixture": torch.empty((B, M, T), dtype=torch.float32, device=dev),
         "sources": torch.empty((B, S, M, T), dtype=torch.float32, device=dev),
