@@ -213,29 +213,24 @@ __device__ __forceinline__ void pair_rows(int pi, int S, int M, int* ja, int* jb
   }
 }
 
-// X_t = FFT of the placed dry signal (speaker k at its offset, or the tiled
-// noise) over [(t-1)P, (t+1)P).  Grid (nb, S+1, B).
-__global__ void __launch_bounds__(kFftThreads, 2) fft_in_kernel(ConvArgs A) {
-  extern __shared__ __align__(16) float2 buf[];
-  const int t = blockIdx.x, k = blockIdx.y, b = blockIdx.z;
-  const float2* tws = load_twiddles(buf, A.tw);
-  const long base = (long)(t - 1) * kFftP;
-  float vals[kFftN / kFftThreads];  // samples base + threadIdx.x + 512 i
+// Samples base + threadIdx.x + 512 i (i < 16) of source k of item b: speaker k
+// placed at its offset, or (k = S) the point noise tiled to the dry length.
+__device__ __forceinline__ void load_block(const ConvArgs& A, int k, int b, long base, float (&vals)[16]) {
   if (k < A.S) {
     const long o = A.off[b * A.S + k], n = A.len[b * A.S + k];
     const float* src = A.dry + (size_t)b * A.dry_sb + (size_t)k * A.dry_sk;
 #pragma unroll
-    for (int i = 0; i < kFftN / kFftThreads; ++i) {
+    for (int i = 0; i < 16; ++i) {
       const long q = base + threadIdx.x + i * kFftThreads - o;
       vals[i] = q >= 0 && q < n ? __ldg(src + q) : 0.f;
     }
-  } else {  // the point noise tiled to the dry length
+  } else {
     const long dl = A.dlen[b], nl = A.nlen[b];
     const float* src = A.noise + (size_t)b * A.noise_sb;
     long pos = base + threadIdx.x;
     long q = pos >= 0 ? pos % nl : 0;
 #pragma unroll
-    for (int i = 0; i < kFftN / kFftThreads; ++i, pos += kFftThreads) {
+    for (int i = 0; i < 16; ++i, pos += kFftThreads) {
       vals[i] = pos >= 0 && pos < dl ? __ldg(src + q) : 0.f;
       if (pos >= 0) {
         q += kFftThreads;
@@ -245,18 +240,80 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_in_kernel(ConvArgs A) {
       }
     }
   }
+}
+
+// Pass 4 of a transform whose input was two real blocks packed as z = a + i b,
+// split into their spectra: X_a[f] = (Z[f] + conj Z[N-f]) / 2 and
+// X_b[f] = (Z[f] - conj Z[N-f]) / 2i.  Thread t takes the butterflies
+// j = t + 512 q (q < 4) and their mirrors P - j (twiddle W^{P-j} = -conj W^j),
+// so Z[f] and Z[N-f] meet in one thread; butterflies 0 and 2048 are their own
+// mirrors (thread 0).  xb may be null (no second block).
+__device__ __forceinline__ void fft_last_real_pair(const float2* buf, const float2* tws, float2* xa, float2* xb) {
+  constexpr float kC[4] = {1.f, 0.92387953251128674f, 0.70710678118654752f, 0.38268343236508977f};
+  constexpr float kS[4] = {0.f, 0.38268343236508977f, 0.70710678118654752f, 0.92387953251128674f};
+  const int t = threadIdx.x;
+  const float2 wt = tws[t];
+  auto bfly = [&](int j, float2 w, float2& z0, float2& z1) {  // Z[j], Z[j + P]
+    const int sj = swz(j);
+    const float2 a = buf[sj], c = cmulf(buf[sj + kFftP], w);
+    z0 = addf(a, c);
+    z1 = subf(a, c);
+  };
+  auto emit = [&](int f, float2 zf, float2 zm) {  // zm = Z[N - f]
+    xa[f] = make_float2(0.5f * (zf.x + zm.x), 0.5f * (zf.y - zm.y));
+    if (xb) xb[f] = make_float2(0.5f * (zf.y + zm.y), 0.5f * (zm.x - zf.x));
+  };
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int j1 = t + 512 * q;
+    const float2 w1 = q == 0 ? wt : cmulc(wt, kC[q], -kS[q]);  // W^{j1}
+    float2 z1a, z1b;
+    bfly(j1, w1, z1a, z1b);
+    if (j1 == 0) {
+      emit(0, z1a, z1a);
+      emit(kFftP, z1b, z1b);
+      float2 za, zb;
+      bfly(2048, make_float2(0.f, -1.f), za, zb);  // W^2048 = -i
+      emit(2048, za, zb);
+      emit(2048 + kFftP, zb, za);
+    } else {
+      const int j2 = kFftP - j1;
+      float2 z2a, z2b;
+      bfly(j2, make_float2(-w1.x, w1.y), z2a, z2b);
+      emit(j1, z1a, z2b);
+      emit(j1 + kFftP, z1b, z2a);
+      emit(j2, z2a, z1b);
+      emit(j2 + kFftP, z2b, z1a);
+    }
+  }
+}
+
+// X_t = FFT of the placed dry signal (speaker k at its offset, or the tiled
+// noise) over [(t-1)P, (t+1)P).  Blocks 2u and 2u + 1 ride in one complex
+// transform (real and imaginary parts).  Grid (ceil(nb / 2), S+1, B).
+__global__ void __launch_bounds__(kFftThreads, 2) fft_in_kernel(ConvArgs A) {
+  extern __shared__ __align__(16) float2 buf[];
+  const int u = blockIdx.x, k = blockIdx.y, b = blockIdx.z;
+  const int t0 = 2 * u;
+  const bool two = t0 + 1 < A.nb;
+  const float2* tws = load_twiddles(buf, A.tw);
   {  // butterfly j = threadIdx.x of pass 1 reads samples j + 512 r
+    float va[16], vb[16];
+    load_block(A, k, b, (long)(t0 - 1) * kFftP, va);
+    if (two) {
+      load_block(A, k, b, (long)t0 * kFftP, vb);
+    } else {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) vb[r] = 0.f;
+    }
     float2 x[16];
 #pragma unroll
-    for (int r = 0; r < 16; ++r) x[r] = make_float2(vals[r], 0.f);
+    for (int r = 0; r < 16; ++r) x[r] = make_float2(va[r], vb[r]);
     fft_first(buf, x);
   }
   fft_mid(buf, tws);
-  float2* out = A.X + (((size_t)b * (A.S + 1) + k) * A.nb + t) * kFftN;
-  fft_last(buf, tws, [&](int j, float2 x0, float2 x1) {
-    out[j] = x0;
-    out[j + kFftP] = x1;
-  });
+  float2* out = A.X + (((size_t)b * (A.S + 1) + k) * A.nb + t0) * kFftN;
+  fft_last_real_pair(buf, tws, out, two ? out + kFftN : nullptr);
 }
 
 // H_p = FFT(h_a + i h_b) over taps [pP, pP + P).  Grid (Q, npairs, B).
@@ -428,7 +485,7 @@ int frir_mix_convolve(const float* dry, int64_t dry_stride_b, int64_t dry_stride
     if (e != cudaSuccess) break;
   }
   if (e == cudaSuccess) {
-    fft_in_kernel<<<dim3(a.nb, S + 1, B), kFftThreads, smem, st>>>(a);
+    fft_in_kernel<<<dim3((a.nb + 1) / 2, S + 1, B), kFftThreads, smem, st>>>(a);
     fft_filt_kernel<<<dim3(a.Q, a.npairs, B), kFftThreads, smem, st>>>(a);
     fft_conv_kernel<<<dim3(a.nb, a.npairs, B), kFftThreads, smem, st>>>(a);
     e = cudaGetLastError();
