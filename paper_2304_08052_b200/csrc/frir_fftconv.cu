@@ -8,9 +8,10 @@
 //   y[tP + n] = last P samples of IFFT( sum_p X_{t-p} . H_p ),  n < P,
 //   X_s = FFT(x[(s-1)P, (s+1)P)),  H_p = FFT(h[pP, pP + P) zero-padded).
 //
-// Two real filter rows that share a source (speaker k: the full and early
-// filters of mic m; the noise: mics m, m+1) ride in one complex transform,
-// H = FFT(h_a + i h_b), so IFFT(X . H) = y_a + i y_b.  The FFT is a radix
+// Two real filter rows that share a source (mics 2h, 2h + 1 of one filter
+// group: a speaker's full filters, its early filters, or the noise) ride in
+// one complex transform, H = FFT(h_a + i h_b), so IFFT(X . H) = y_a + i y_b;
+// all-zero filter partitions (early filters end early) are skipped.  The FFT is a radix
 // 16 * 16 * 16 * 2 Stockham in place in 64 KB of swizzled shared memory, 512
 // threads, twiddles from an FP64-computed table.  FP32 throughout (the
 // reference is FP64; the mixing tests hold the result to 1e-5 of the peak).
@@ -191,26 +192,34 @@ struct ConvArgs {
   long early_sb;
   const int32_t* rlen;
   int S, M, R, nb, Q, npairs;
+  int hm;      // row pairs per filter group: ceil(M / 2)
   const float2* tw;
   float2* X;   // [B][S+1][nb][N]
   float2* H;   // [B][npairs][Q][N]
+  int32_t* live;  // [B][npairs][Q]: partition has a non-zero tap
   float* y;    // [B][J][y_stride]
   long y_stride;
 };
 
-// pair -> (row a, row b or -1, source)
-__device__ __forceinline__ void pair_rows(int pi, int S, int M, int* ja, int* jb, int* src) {
-  if (pi < S * M) {
-    const int k = pi / M, m = pi % M;
-    *ja = k * M + m;          // full filter, speaker k, mic m
-    *jb = (S + k) * M + m;    // early filter
-    *src = k;
-  } else {
-    const int m = 2 * (pi - S * M);
-    *ja = 2 * S * M + m;      // noise filters, mics m and m + 1
-    *jb = m + 1 < M ? 2 * S * M + m + 1 : -1;
-    *src = S;
-  }
+// Row pairs: filter group g (g < S: full filters of speaker g, S <= g < 2S:
+// early filters of speaker g - S, g = 2S: the noise) pairs mics 2h and 2h + 1,
+// so both rows of a pair convolve the same source and the short early
+// filters pair with each other (their zero partitions are skipped).  Without
+// early filters the early groups are not run: the full pair writes both.
+struct Pair {
+  int ja, jb, src;  // rows (jb = -1: no partner) and source
+  bool dup;         // also write rows ja + S M, jb + S M (early == full)
+};
+__device__ __forceinline__ Pair pair_rows(int pi, const ConvArgs& A) {
+  int g = pi / A.hm;
+  const int h = pi - g * A.hm;
+  if (!A.rir_early && g >= A.S) g += A.S;
+  Pair P;
+  P.ja = g * A.M + 2 * h;
+  P.jb = 2 * h + 1 < A.M ? P.ja + 1 : -1;
+  P.src = g < A.S ? g : g < 2 * A.S ? g - A.S : A.S;
+  P.dup = !A.rir_early && g < A.S;
+  return P;
 }
 
 // Samples base + threadIdx.x + 512 i (i < 16) of source k of item b: speaker k
@@ -322,8 +331,8 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_filt_kernel(ConvArgs A) {
   const int p = blockIdx.x, pi = blockIdx.y, b = blockIdx.z;
   const int M = A.M, S = A.S, r = A.rlen[b];
   if (p * kFftP >= r) return;  // partitions past this item's filter length are never read
-  int ja, jb, src;
-  pair_rows(pi, A.S, A.M, &ja, &jb, &src);
+  const Pair pr = pair_rows(pi, A);
+  const int ja = pr.ja, jb = pr.jb;
   auto row = [&](int j) -> const float* {
     if (j < S * M) return A.rir_full + (size_t)b * A.full_sb + (size_t)j * A.R;
     if (j < 2 * S * M) {
@@ -349,6 +358,12 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_filt_kernel(ConvArgs A) {
       }
       x[q] = make_float2(va, vb);
     }
+    bool nz = false;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) nz |= x[q].x != 0.f || x[q].y != 0.f;
+    const bool live = __syncthreads_or(nz);
+    if (threadIdx.x == 0) A.live[((size_t)b * A.npairs + pi) * A.Q + p] = live;
+    if (!live) return;  // all-zero partition (the tail of an early filter): skipped by the convolution
     fft_first(buf, x);
   }
   fft_mid(buf, tws);
@@ -364,9 +379,10 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_filt_kernel(ConvArgs A) {
 __global__ void __launch_bounds__(kFftThreads, 2) fft_conv_kernel(ConvArgs A) {
   extern __shared__ __align__(16) float2 buf[];
   const int t = blockIdx.x, pi = blockIdx.y, b = blockIdx.z;
-  int ja, jb, src;
-  pair_rows(pi, A.S, A.M, &ja, &jb, &src);
-  const float2* Xs = A.X + ((size_t)b * (A.S + 1) + src) * A.nb * kFftN;
+  const Pair pr = pair_rows(pi, A);
+  const int ja = pr.ja, jb = pr.jb;
+  const float2* Xs = A.X + ((size_t)b * (A.S + 1) + pr.src) * A.nb * kFftN;
+  const int32_t* live = A.live + ((size_t)b * A.npairs + pi) * A.Q;
   const float2* Hs = A.H + ((size_t)b * A.npairs + pi) * A.Q * kFftN;
   const int qb = (A.rlen[b] + kFftP - 1) / kFftP;  // this item's non-zero partitions
   const int qmax = min(qb - 1, t);
@@ -377,6 +393,7 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_conv_kernel(ConvArgs A) {
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = make_float2(0.f, 0.f);
     for (int p = 0; p <= qmax; ++p) {
+      if (!live[p]) continue;  // block-uniform
       const float2* xp = Xs + (size_t)(t - p) * kFftN + j;
       const float2* hp = Hs + (size_t)p * kFftN + j;
 #pragma unroll
@@ -402,9 +419,14 @@ __global__ void __launch_bounds__(kFftThreads, 2) fft_conv_kernel(ConvArgs A) {
   const float inv = 1.0f / kFftN;
   float* ya = A.y + ((size_t)b * ((2 * A.S + 1) * A.M) + ja) * A.y_stride + (size_t)t * kFftP;
   float* yb = jb >= 0 ? A.y + ((size_t)b * ((2 * A.S + 1) * A.M) + jb) * A.y_stride + (size_t)t * kFftP : nullptr;
+  const size_t dup = pr.dup ? (size_t)A.S * A.M * A.y_stride : 0;  // early rows = full rows
   fft_last(buf, tws, [&](int n, float2, float2 z1) {  // the last P outputs: X[n + P]
     ya[n] = z1.x * inv;
     if (yb) yb[n] = -z1.y * inv;
+    if (dup) {
+      ya[dup + n] = z1.x * inv;
+      if (yb) yb[dup + n] = -z1.y * inv;
+    }
   });
 }
 
@@ -442,9 +464,10 @@ int64_t frir_mix_convolve_scratch(int32_t B, int32_t S, int32_t M, int64_t R, in
   if (B < 0 || S < 1 || M < 1 || R < 1 || T < 1) return -1;
   const int64_t nb = (T + kFftP - 1) / kFftP;
   const int64_t Q = (R + kFftP - 1) / kFftP;
-  const int64_t npairs = (int64_t)S * M + (M + 1) / 2;
+  const int64_t npairs = (int64_t)(2 * S + 1) * ((M + 1) / 2);
   if (y_stride) *y_stride = nb * kFftP;
-  return ((int64_t)B * (S + 1) * nb + (int64_t)B * npairs * Q) * kFftN * (int64_t)sizeof(float2);
+  const int64_t flags = ((int64_t)B * npairs * Q * 4 + 255) & ~(int64_t)255;
+  return ((int64_t)B * (S + 1) * nb + (int64_t)B * npairs * Q) * kFftN * (int64_t)sizeof(float2) + flags;
 }
 
 int frir_mix_convolve(const float* dry, int64_t dry_stride_b, int64_t dry_stride_k, const float* noise,
@@ -472,10 +495,12 @@ int frir_mix_convolve(const float* dry, int64_t dry_stride_b, int64_t dry_stride
   a.S = S; a.M = M; a.R = (int)R;
   a.nb = (int)((T + kFftP - 1) / kFftP);
   a.Q = (int)((R + kFftP - 1) / kFftP);
-  a.npairs = S * M + (M + 1) / 2;
+  a.hm = (M + 1) / 2;
+  a.npairs = (rir_early ? 2 * S + 1 : S + 1) * a.hm;  // no early filters: the full pairs write both
   a.tw = tw;
   a.X = (float2*)scratch;
   a.H = a.X + (size_t)B * (S + 1) * a.nb * kFftN;
+  a.live = (int32_t*)(a.H + (size_t)B * a.npairs * a.Q * kFftN);
   a.y = y; a.y_stride = (long)y_stride;
   const size_t smem = kFftSmem;
   cudaStream_t st = (cudaStream_t)stream;

@@ -29,7 +29,8 @@ def test_spec_validation(kw, msg):
 def test_convolve_scratch_sizes():
     """frir_mix_convolve_scratch (host-side sizing, no GPU): spectra of every
     4096-sample block of each source plus every filter partition of each row
-    pair, 8192 complex64 bins each; y rows padded to whole blocks."""
+    pair (mics 2h, 2h + 1 of each filter group), 8192 complex64 bins each, and
+    the partitions' non-zero flags; y rows padded to whole blocks."""
     import ctypes
 
     from paper_2304_08052_b200 import _abi
@@ -38,9 +39,10 @@ def test_convolve_scratch_sizes():
     ys = ctypes.c_int64(0)
     B, S, M, R, T = 3, 2, 4, 9000, 70000
     got = lib.frir_mix_convolve_scratch(B, S, M, R, T, ctypes.byref(ys))
-    nb, q, pairs = -(-T // 4096), -(-R // 4096), S * M + (M + 1) // 2
+    nb, q, pairs = -(-T // 4096), -(-R // 4096), (2 * S + 1) * ((M + 1) // 2)
     assert ys.value == nb * 4096
-    assert got == (B * (S + 1) * nb + B * pairs * q) * 8192 * 8
+    flags = (B * pairs * q * 4 + 255) // 256 * 256  # one int32 per filter partition: non-zero taps
+    assert got == (B * (S + 1) * nb + B * pairs * q) * 8192 * 8 + flags
     lib.frir_mix_convolve_scratch(1, 1, 3, 1, 1, ctypes.byref(ys))
     assert ys.value == 4096
     assert lib.frir_mix_convolve_scratch(1, 0, 4, 10, 10, None) == -1
