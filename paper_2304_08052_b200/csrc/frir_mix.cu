@@ -24,17 +24,22 @@ __global__ void mix_power_kernel(const float* __restrict__ y, const int64_t* __r
                                  const int32_t* __restrict__ req_lo, const int32_t* __restrict__ req_hi,
                                  long F, double* __restrict__ part) {
   const int r = blockIdx.y, c = blockIdx.x;
-  const float* row = y + (size_t)req_row[r] * F;
+  const float* __restrict__ row = y + (size_t)req_row[r] * F;
   const int lo = req_lo[r], hi = req_hi[r];
   const int span = (hi - lo + kPowChunks - 1) / kPowChunks;
   const int a = lo + c * span, e = min(hi, a + span);
-  double acc = 0.0;
-  for (int t = a + threadIdx.x; t < e; t += blockDim.x) {
-    const double v = (double)row[t];
-    acc = fma(v, v, acc);
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};  // four independent loads in flight per thread
+  int t = a + threadIdx.x;
+  for (; t + 3 * 256 < e; t += 4 * 256) {
+    float v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = row[t + i * 256];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i] = fma((double)v[i], (double)v[i], acc[i]);
   }
+  for (int i = 0; t < e; t += 256, ++i) acc[i] = fma((double)row[t], (double)row[t], acc[i]);
   __shared__ double s[256];
-  s[threadIdx.x] = acc;
+  s[threadIdx.x] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
   __syncthreads();
   for (int o = blockDim.x / 2; o > 0; o >>= 1) {
     if ((int)threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
