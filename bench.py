@@ -375,6 +375,11 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "RIR/s", "h2d_bytes_per_step": e2e["h2d"],
                 "d2h_bytes_per_step": e2e["d2h"], "ms_per_step": e2e_ms,
+                "link": {"achieved_gbs": (e2e["h2d"] + e2e["d2h"]) / (e2e_ms / 1e3) / 1e9,
+                         "d2h_peak_gbs": e2e["d2h_peak_gbs"],
+                         "frac": (e2e["h2d"] + e2e["d2h"]) / (e2e_ms / 1e3) / 1e9 / e2e["d2h_peak_gbs"],
+                         "note": "host<->device bytes per step / e2e step time vs a pinned D2H copy of the "
+                                 "same size"},
                 "path": "engine.HostPipeline: frir_jobs_prepare + H2D(job tables) + frir_simulate + "
                         "D2H(all RIRs) to pinned host, 4 chunks, copy overlapped with render"},
         "gpu_launches": launches_per_step * K,
@@ -399,7 +404,28 @@ def run_e2e(args, batch, early, dev, stream):
     for _ in range(steps):
         pipe.run()
     ms = (time.perf_counter() - t0) * 1e3 / steps
-    return {"ms_per_step": ms, "h2d": int(pipe.h2d_bytes), "d2h": int(pipe.d2h_bytes)}
+    return {"ms_per_step": ms, "h2d": int(pipe.h2d_bytes), "d2h": int(pipe.d2h_bytes),
+            "d2h_peak_gbs": d2h_peak_gbs(int(pipe.d2h_bytes), dev)}
+
+
+def d2h_peak_gbs(nbytes, dev):
+    """Device -> pinned host copy bandwidth for one block of `nbytes` (best of
+    3, CUDA events): the PCIe ceiling of the end-to-end path."""
+    import torch
+
+    n = max(nbytes, 1 << 20)
+    src = torch.empty(n, dtype=torch.uint8, device=dev)
+    dst = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    best = None
+    for _ in range(4):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dst.copy_(src, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = ms if best is None else min(best, ms)
+    return n / (best / 1e3) / 1e9
 
 
 def torch_sync(dev):

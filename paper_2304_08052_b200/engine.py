@@ -236,6 +236,10 @@ class HostPipeline:
             nfl = int(pb.batch.total_out)
             host = {
                 "jobs": torch.empty(pb.jobs.nbytes, dtype=torch.uint8).pin_memory(),
+                # the other per-chunk tables, staged pinned so every H2D is asynchronous
+                "chan_job": torch.empty(len(pb.chan_job), dtype=torch.int32).pin_memory(),
+                "chan_order": torch.empty(len(pb.chan_order), dtype=torch.int32).pin_memory(),
+                "mics": torch.empty(pb.mics.size, dtype=torch.float64).pin_memory(),
                 "full": torch.empty(nfl, dtype=torch.float32).pin_memory(),
                 "early": torch.empty(nfl, dtype=torch.float32).pin_memory() if include_early else None,
                 "direct": torch.empty(int(pb.batch.total_channels), dtype=torch.int32).pin_memory(),
@@ -272,11 +276,14 @@ class HostPipeline:
             if revalidate:  # host validation + layout, as a caller with fresh rooms would do
                 pb = prepare(self.sample_rate, self.jobs_src[lo:hi], self.mics_src)
             host["jobs"].numpy()[:] = pb.jobs.view(np.uint8).reshape(-1)
+            host["chan_job"].numpy()[:] = pb.chan_job
+            host["chan_order"].numpy()[:] = pb.chan_order
+            host["mics"].numpy()[:] = pb.mics.reshape(-1)
             with torch.cuda.stream(self.compute):
                 db.jobs.copy_(host["jobs"], non_blocking=True)
-                db.chan_job.copy_(torch.from_numpy(pb.chan_job), non_blocking=True)
-                db.chan_order.copy_(torch.from_numpy(pb.chan_order), non_blocking=True)
-                db.mics.copy_(torch.from_numpy(pb.mics.reshape(-1)), non_blocking=True)
+                db.chan_job.copy_(host["chan_job"], non_blocking=True)
+                db.chan_order.copy_(host["chan_order"], non_blocking=True)
+                db.mics.copy_(host["mics"], non_blocking=True)
                 db.launch(full, early, direct, self.compute)
                 ev = torch.cuda.Event()
                 ev.record(self.compute)
