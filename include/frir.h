@@ -276,7 +276,8 @@ int frir_sample_scene_jobs(const frir_plan* plan, const frir_scene_spec* spec, u
    Rows h[c][0:len[c]] (float32, row stride ld floats).  frir_edc writes the
    unnormalised energy decay curve edc[c][i] = sum_{j>=i} h[c][j]^2 in FP64,
    summed sequentially from the end exactly like numpy's cumsum of the
-   reversed squares (bit-identical), and amax[c] = max |h[c]|. */
+   reversed squares (bit-identical), zeros for len[c] <= i < ld_out, and
+   amax[c] = max |h[c]|. */
 int frir_edc(const float* h, int64_t ld, const int32_t* len, int32_t C, double* edc, int64_t ld_out,
              double* amax, void* stream);
 /* measure_t60 (decay.py:20-49) per row from frir_edc's outputs: NaN when the

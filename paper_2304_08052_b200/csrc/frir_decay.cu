@@ -1,10 +1,12 @@
 // sm_100a kernels of the batched decay measurement:
 // reference framrir/decay.py:8-49 (schroeder_curve, measure_t60).
 //
-// One thread per channel walks its row backwards in FP64 exactly like
-// numpy's sequential cumsum of the reversed squared response, so the energy
-// decay curve is bit-identical to the reference's; rows are staged through
-// shared memory in 32-sample tiles so the global loads stay coalesced.  The
+// One lane per channel walks its row backwards in FP64 exactly like numpy's
+// sequential cumsum of the reversed squared response, so the energy decay
+// curve is bit-identical to the reference's; rows are staged through shared
+// memory in 64-sample tiles both ways (a cp.async ring in, row-contiguous
+// stores out) by a second warp, so loads and stores stay coalesced and off
+// the serial sums.  The
 // T60 kernel then finds the direct-path index, the adaptive drop and the
 // first crossing (binary search: the curve is monotone) per channel.
 #include <cuda_runtime.h>
@@ -18,54 +20,140 @@
 namespace frir {
 namespace {
 
-constexpr int kEdcThreads = 128;  // channels per CTA
-constexpr int kEdcTile = 32;      // samples per staged tile
+constexpr int kEdcRows = 32;    // channels per CTA; lane = channel in the sums
+constexpr int kEdcTile = 64;    // samples per staged tile
+constexpr int kEdcStages = 8;   // input tiles in flight (cp.async ring)
+constexpr int kEdcIn = kEdcTile + 4;   // padded input row: 16-byte aligned, 4-way banks
+constexpr int kEdcOut = kEdcTile + 2;  // padded output row: 16-byte aligned
+constexpr int kEdcIo = 4;               // I/O warps per CTA (plus one summing warp)
+constexpr size_t kEdcSmem = (size_t)kEdcStages * kEdcRows * kEdcIn * 4 + 2 * (size_t)kEdcRows * kEdcOut * 8 +
+                            kEdcRows * 4;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 // edc[c][i] = sum_{j >= i} h[c][j]^2 (FP64, sequential from the end) for
-// i < len[c]; amax[c] = max |h[c][i]|.  Rows are float32 with stride `ld`.
-__global__ void __launch_bounds__(kEdcThreads) edc_kernel(const float* __restrict__ h, long ld,
-                                                        const int32_t* __restrict__ len, int C,
-                                                        double* __restrict__ edc, long ld_out,
-                                                        double* __restrict__ amax) {
-  __shared__ float tile[kEdcThreads][kEdcTile + 1];
-  const int c0 = blockIdx.x * kEdcThreads;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int c = c0 + threadIdx.x;
-  const int n = c < C ? len[c] : 0;
-  // longest row of the CTA (tiles run to its start)
-  int nmax = n;
-  for (int o = 16; o > 0; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
-  __shared__ int s_nmax[kEdcThreads / 32];
-  if (lane == 0) s_nmax[warp] = nmax;
+// i < len[c], zeros for len[c] <= i < ld_out; amax[c] = max |h[c][i]|.  Rows
+// are float32 with stride `ld`.  Per 32 channels, warp 0 runs each lane's row
+// sum in numpy's order over tiles of 64 samples; four I/O warps stream the
+// tiles in through an 8-deep cp.async ring (16-byte row-contiguous copies,
+// zero-filled past each length; scalar loads when rows are not 16-byte
+// aligned) and writes the previous EDC tile out row-contiguous, so the serial
+// sums never wait on memory.
+__global__ void __launch_bounds__(32 * (1 + kEdcIo)) edc_kernel(const float* __restrict__ h, long ld,
+                                                 const int32_t* __restrict__ len, int C,
+                                                 double* __restrict__ edc, long ld_out,
+                                                 double* __restrict__ amax) {
+  extern __shared__ __align__(16) unsigned char edc_smem[];
+  float(*tin)[kEdcRows][kEdcIn] = reinterpret_cast<float(*)[kEdcRows][kEdcIn]>(edc_smem);
+  double(*tout)[kEdcRows][kEdcOut] =
+      reinterpret_cast<double(*)[kEdcRows][kEdcOut]>(edc_smem + (size_t)kEdcStages * kEdcRows * kEdcIn * 4);
+  int* s_len = reinterpret_cast<int*>(edc_smem + (size_t)kEdcStages * kEdcRows * kEdcIn * 4 +
+                                      2 * (size_t)kEdcRows * kEdcOut * 8);
+  const int c0 = blockIdx.x * kEdcRows;
+  const int lane = threadIdx.x & 31;
+  const bool io = threadIdx.x >= 32;
+  const int iw = (threadIdx.x >> 5) - 1;  // I/O warp index
+  if (!io) s_len[lane] = c0 + lane < C ? len[c0 + lane] : 0;
   __syncthreads();
-  nmax = 0;
-  for (int w = 0; w < kEdcThreads / 32; ++w) nmax = max(nmax, s_nmax[w]);
-  double acc = 0.0, mx = 0.0;
-  const int ntile = (nmax + kEdcTile - 1) / kEdcTile;
-  for (int t = ntile - 1; t >= 0; --t) {
-    const int base = t * kEdcTile;
-    __syncthreads();
-    // warp w stages rows w, w + 4, ...: lane = sample within the tile (coalesced)
-    for (int r = warp; r < kEdcThreads; r += kEdcThreads / 32) {
-      const int cr = c0 + r;
-      float v = 0.f;
-      if (cr < C && base + lane < len[cr]) v = h[(size_t)cr * ld + base + lane];
-      tile[r][lane] = v;
-    }
-    __syncthreads();
-    if (c < C) {
-      for (int k = kEdcTile - 1; k >= 0; --k) {
-        const int i = base + k;
-        if (i < n) {
-          const double v = (double)tile[threadIdx.x][k];
-          acc += v * v;  // numpy: cumsum(h[::-1] ** 2), sequential
-          edc[(size_t)c * ld_out + i] = acc;
-          mx = fmax(mx, fabs(v));
+  int nmax = 0;
+  for (int r = 0; r < kEdcRows; ++r) nmax = max(nmax, s_len[r]);
+  const int ntile = (int)((max((long)nmax, ld_out) + kEdcTile - 1) / kEdcTile);
+  const int nlive = (nmax + kEdcTile - 1) / kEdcTile;  // tiles holding samples
+  const bool vec_in = (ld % 4 == 0) && (((uintptr_t)h & 15) == 0);
+  const bool vec_out = (ld_out % 2 == 0) && (((uintptr_t)edc & 15) == 0);
+
+  auto stage = [&](int t) {  // I/O warp: tile t into ring slot t % kEdcStages
+    if (t >= 0 && t < nlive) {
+      const int base = t * kEdcTile;
+      float(*dst)[kEdcIn] = tin[t % kEdcStages];
+#pragma unroll
+      for (int i = 0; i < kEdcRows * kEdcTile / 4 / (32 * kEdcIo); ++i) {
+        const int q = (i * kEdcIo + iw) * 32 + lane, r = q >> 4, col = (q & 15) * 4;
+        const int nr = s_len[r];
+        const long off = (long)(c0 + r) * ld + base + col;
+        if (vec_in) {
+          const int bytes = max(0, min(16, (nr - base - col) * 4));
+          cp_async16(&dst[r][col], bytes > 0 ? (const void*)(h + off) : (const void*)h, bytes);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) dst[r][col + e] = base + col + e < nr ? h[off + e] : 0.f;
         }
       }
     }
+    cp_async_commit();
+  };
+  auto store = [&](int t) {  // I/O warp: EDC tile t (zeros for tiles past every length)
+    if (t < 0 || t >= ntile) return;
+    const int base = t * kEdcTile, k2 = 2 * lane;
+    for (int r = iw; r < kEdcRows && c0 + r < C; r += kEdcIo) {
+      double* out = edc + (size_t)(c0 + r) * ld_out + base;
+      const double2 v = t < nlive ? *reinterpret_cast<const double2*>(&tout[t & 1][r][k2]) : make_double2(0.0, 0.0);
+      if (vec_out && base + k2 + 1 < ld_out) {
+        *reinterpret_cast<double2*>(out + k2) = v;
+      } else {
+        if (base + k2 < ld_out) out[k2] = v.x;
+        if (base + k2 + 1 < ld_out) out[k2 + 1] = v.y;
+      }
+    }
+  };
+
+  if (io) {
+    for (int k = 0; k < kEdcStages - 1; ++k) stage(nlive - 1 - k);
+    cp_async_wait<kEdcStages - 2>();  // tile nlive - 1 has landed
+    __syncwarp();
   }
-  if (c < C) amax[c] = mx;
+  double acc = 0.0;
+  float mx = 0.f;  // |h| is a float: the max is exact in FP32
+  for (int t = ntile - 1; t >= -1; --t) {
+    __syncthreads();  // tile t staged; tout[t & 1] free (its store was two rounds ago)
+    if (!io) {
+      if (t >= 0 && t < nlive) {
+        const float(*src)[kEdcIn] = tin[t % kEdcStages];
+        double* dst = tout[t & 1][lane];
+        // No length tests: samples past a row's end were staged as zeros and
+        // come first in the backward walk, so they leave acc at +0.0 and
+        // their EDC entries are the zeros the contract asks for.
+        // Warps issue in order: the independent loads, conversions and
+        // squares of a half tile go first, then the dependent adds back to
+        // back (one FP64 add latency per sample).
+#pragma unroll
+        for (int hh = 1; hh >= 0; --hh) {
+          double sq[kEdcTile / 2];
+#pragma unroll
+          for (int k = 0; k < kEdcTile / 2; k += 4) {  // 16-byte reads: conflict-free per quarter warp
+            const float4 f4 = *reinterpret_cast<const float4*>(&src[lane][hh * (kEdcTile / 2) + k]);
+            const float f[4] = {f4.x, f4.y, f4.z, f4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const double v = (double)f[e];
+              sq[k + e] = v * v;
+              mx = fmaxf(mx, fabsf(f[e]));
+            }
+          }
+#pragma unroll
+          for (int k = kEdcTile / 2 - 2; k >= 0; k -= 2) {
+            const double a1 = acc + sq[k + 1];  // numpy: cumsum(h[::-1] ** 2), sequential
+            acc = a1 + sq[k];
+            *reinterpret_cast<double2*>(&dst[hh * (kEdcTile / 2) + k]) = make_double2(acc, a1);
+          }
+        }
+      }
+    } else {
+      store(t + 1);                        // the tile computed last round
+      if (t >= 0 && t < nlive) {
+        stage(t - (kEdcStages - 1));       // keep the ring full
+        cp_async_wait<kEdcStages - 2>();   // tile t - 1 has landed
+      }
+      __syncwarp();
+    }
+  }
+  if (!io && c0 + lane < C) amax[c0 + lane] = (double)mx;
 }
 
 __device__ __forceinline__ double db_of(double e, double e0) {
@@ -119,7 +207,9 @@ int frir_edc(const float* h, int64_t ld, const int32_t* len, int32_t C, double* 
     return FRIR_EINVAL;
   }
   if (C == 0) return FRIR_OK;
-  edc_kernel<<<(C + kEdcThreads - 1) / kEdcThreads, kEdcThreads, 0, (cudaStream_t)stream>>>(
+  // > 48 KB of dynamic shared memory (per device and function: set every call)
+  cudaFuncSetAttribute(edc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEdcSmem);
+  edc_kernel<<<(C + kEdcRows - 1) / kEdcRows, 32 * (1 + kEdcIo), kEdcSmem, (cudaStream_t)stream>>>(
       h, (long)ld, len, C, edc, (long)ld_out, amax);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { set_error(std::string("edc_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }

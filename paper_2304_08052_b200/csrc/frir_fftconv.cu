@@ -89,18 +89,6 @@ __device__ __forceinline__ void dft16(const float2 (&x)[16], float2 (&o)[16]) {
 __device__ __forceinline__ int swz(int i) { return i ^ ((i >> 4) & 15); }
 constexpr int kTwN = kFftN / 8;  // smem twiddle table: W^m, m < N / 8
 
-// W^m for m < N / 2 from the eighth-circle table: W^{m mod N/8} times the
-// rotation e^{-i pi/4 * (m div N/8)}.
-__device__ __forceinline__ float2 twiddle_half(const float2* tws, int m) {
-  const float2 lo = tws[m & (kTwN - 1)];
-  const int e = m / kTwN;  // 0..3
-  const float c = 0.70710678118654752f;
-  const float2 rot = e == 0 ? make_float2(1.f, 0.f)
-                   : e == 1 ? make_float2(c, -c)
-                   : e == 2 ? make_float2(0.f, -1.f) : make_float2(-c, -c);
-  return cmulf(lo, rot);
-}
-
 // The forward 8192-point FFT is a radix 16 * 16 * 16 * 2 Stockham
 // decomposition, 512 threads, one butterfly per thread per radix-16 pass:
 //   fft_first(buf, x): pass 1 of butterfly j = threadIdx.x from registers,

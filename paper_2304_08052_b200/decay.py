@@ -45,7 +45,7 @@ def _rows(h, lengths, device):
 def _edc(h, lens, dev):
     torch = _torch()
     C, n = h.shape
-    edc = torch.zeros((C, n), dtype=torch.float64, device=dev)
+    edc = torch.empty((C, n), dtype=torch.float64, device=dev)  # frir_edc zero-fills past each length
     amax = torch.empty(C, dtype=torch.float64, device=dev)
     st = torch.cuda.current_stream(dev).cuda_stream
     _abi.check(_abi.lib().frir_edc(h.data_ptr(), h.stride(0), lens.data_ptr(), C, edc.data_ptr(), n,

@@ -110,3 +110,36 @@ def test_mixture_port_matches_reference(golden, ci):
         assert np.abs(pe[k] - ref["early"][k]).max() / pk < 1e-6
     assert np.abs(nimg - ref["noise"]).max() / pk < 1e-6
     assert np.allclose(gains, m["gains"], rtol=1e-12) and math.isclose(gn, m["noise_gain"], rel_tol=1e-12)
+
+
+@pytest.mark.parametrize("ci", range(5))
+def test_ism_port_matches_reference(golden, ci):
+    """oracle/ism_port vs framrir.ism.ism_rir (tests/golden/ism.*)."""
+    from oracle import ism_port as IP
+
+    m = golden["ism_meta"][ci]
+    c = m["cfg"]
+    full, direct = IP.render(c["room_dims"], c["source_position"], c["mic_positions"], c["t60"],
+                             sample_rate=c.get("sample_rate", 16000), order=c.get("max_order"),
+                             duration=c.get("duration"), reflection=c.get("reflection"))
+    ref = golden["ism"][f"c{ci}_samples"]
+    assert full.shape == ref.shape
+    assert np.abs(full.astype(np.float32) - ref).max() <= 1e-6 * m["peak"]
+    assert np.array_equal(direct, golden["ism"][f"c{ci}_direct"])
+    assert IP.eyring(c["room_dims"], c["t60"]) == m["metadata"]["reflection_coefficient"] or "reflection" in c
+
+
+def test_decay_port_matches_reference(golden):
+    """oracle/decay_port vs framrir.decay (tests/golden/decay.*): EDC values
+    bit for bit, T60 exactly."""
+    from _decaycases import rows
+
+    from oracle import decay_port as DP
+
+    d = golden["decay"]
+    for i, r in enumerate(rows(golden)):
+        c = DP.schroeder(r)
+        assert np.array_equal(c[d[f"edc_idx{i}"]], d[f"edc{i}"]), i
+        t = DP.t60(r, 16000)
+        ref = golden["decay_meta"]["t60"][i]
+        assert (ref is None and math.isnan(t)) or t == ref, i
