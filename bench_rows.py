@@ -4,9 +4,9 @@ and 4); one JSON line each.
 ism    -- the GPU image-source method on the reference's own ISM benchmark
           workload (framrir/bench.py:116-158 bench_ism: MixtureSpec rooms,
           3 sources per room uniform in [0.3, L - 0.3], the mic array at the
-          room centre, max_order resolved from c0 * T60).  value: RIRs/s with
-          the lattice rows resident in HBM; e2e: ism.ism_batch (host lattice
-          + H2D + render + D2H to numpy); cpu_baseline: oracle/ism_port (the
+          room centre, max_order resolved from c0 * T60).  value: RIRs/s of
+          the device launch (lattice enumerated in K1); e2e: ism.ism_batch
+          (job table + H2D + render + D2H to numpy); cpu_baseline: oracle/ism_port (the
           reference's dense np.add.at + scipy chain) on a bounded sample, one
           process per core.
 decay  -- batched Schroeder curves + T60 (frir_edc + frir_t60) over the
@@ -103,11 +103,11 @@ def bench_ism(a, torch, dev):
         "data": "synthetic: MixtureSpec rooms (sample_scene draws), sources uniform in [0.3, L - 0.3]",
         "config": {"workload": f"{len(cfgs)} ISM RIRs ({a.ism_rooms} rooms x 3 sources, 4 mics, 16 kHz, "
                                f"max_order from c0*T60), {n_items / len(cfgs) / 4:.0f} lattice images per RIR "
-                               "after the reach cull", "items_per_step": n_items},
+                               "enumerated on the device", "items_per_step": n_items},
         "e2e": {"value": len(cfgs) / wall, "unit": "RIR/s", "ms_per_step": wall * 1e3,
-                "h2d_bytes_per_step": int(sum(d.nbytes for d in draws) + jobs.nbytes + mics.nbytes),
+                "h2d_bytes_per_step": int(jobs.nbytes + mics.nbytes + (sum(d.nbytes for d in draws) if draws else 0)),
                 "d2h_bytes_per_step": int(full.numel() * 4 + direct.numel() * 4),
-                "path": "ism.ism_batch: host lattice + cull, H2D of the lattice rows, render, D2H to numpy"},
+                "path": "ism.ism_batch: job table H2D, lattice enumerated on the device, render, D2H to numpy"},
         "gpu_launches": int(engine_launches(db, False)) * a.steps,
     }
     if not a.no_cpu_baseline:

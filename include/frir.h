@@ -97,7 +97,7 @@ typedef struct {
   int32_t n_images_hi;       /* > n_images: I ~ U{n_images..n_images_hi} from stream (seed, k, 2) */
   int32_t normalize;         /* 0: reference scaling; 1: direct path of every channel = 1/1 m (x D_0m) */
   int32_t kind;              /* FRIR_KIND_FRAM (0) or FRIR_KIND_ISM (1), see below */
-  int32_t pad2_;
+  int32_t lattice;           /* ISM: 1 + max_order to generate the image lattice on the device (0: images as batch draws) */
   double early_lo_ms;        /* early window [-lo, +hi] ms around the direct path; 0/0 means 6/50 */
   double early_hi_ms;
   double duration;           /* ISM: train length in s (0: t60), ism.py:39-60 */
@@ -121,12 +121,15 @@ typedef struct {
 } frir_job;
 
 /* Job kinds.  FRIR_KIND_ISM runs the shoebox image-source reference
-   (ism.py:81-147, ism_rir) through the same chain: the images are given as
-   batch draws (draw_dist, draw_az, draw_el = ABSOLUTE x, y, z of image i,
-   draw_refl = its integer reflection count g), row 0 is the source itself at
-   `center` (d0 = 0), gains are r^g / D with r = exp(-0.0805 V/S/t60)
-   (ism.py:63-78) unless `reflection` > 0, and arrivals past the train end are
-   dropped instead of clamped (ism.py:131-133).  Full variant only. */
+   (ism.py:81-147, ism_rir) through the same chain.  Row 0 is the source
+   itself at `center` (d0 = 0); the images are either generated on the device
+   (`lattice` = K + 1: the (2K + 1)^3 - 1 lattice points of enumerate_images,
+   ism.py:80-104, in its order without the origin; frir_jobs_prepare sets
+   n_images) or given as batch draws (draw_dist, draw_az, draw_el = ABSOLUTE
+   x, y, z of image i, draw_refl = its integer reflection count g).  Gains are
+   r^g / D with r = exp(-0.0805 V/S/t60) (ism.py:63-78) unless `reflection`
+   > 0, and arrivals past the train end are dropped instead of clamped
+   (ism.py:131-133).  Full variant only. */
 enum { FRIR_KIND_FRAM = 0, FRIR_KIND_ISM = 1 };
 
 typedef struct {

@@ -45,7 +45,7 @@ class FrirJob(ctypes.Structure):
         ("beta", c_double), ("perturb_lo", c_double), ("perturb_hi", c_double), ("tau", c_double),
         ("seed", c_uint64), ("source_index", c_int32), ("n_images", c_int32),
         ("mic_off", c_int32), ("n_mics", c_int32),
-        ("n_images_hi", c_int32), ("normalize", c_int32), ("kind", c_int32), ("pad2_", c_int32),
+        ("n_images_hi", c_int32), ("normalize", c_int32), ("kind", c_int32), ("lattice", c_int32),
         ("early_lo_ms", c_double), ("early_hi_ms", c_double), ("duration", c_double),
         ("reflection", c_double),
         ("img_off", c_int64), ("item_off", c_int64), ("out_off", c_int64),

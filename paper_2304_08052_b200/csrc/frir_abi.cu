@@ -227,6 +227,16 @@ int frir_jobs_prepare(int32_t sample_rate, frir_job* jobs, int32_t n_jobs, int32
       for (int k = 0; k < 3; ++k)
         if (!(J.room[k] > 0)) { set_error(pre + "room_dims must be 3 positive lengths"); return FRIR_EINVAL; }
       if (J.n_mics < 1) { set_error(pre + "mic_positions must be an (M, 3) array with M >= 1"); return FRIR_EINVAL; }
+      if (J.lattice < 0) { set_error(pre + "max_order must be >= 0"); return FRIR_EINVAL; }
+      if (J.lattice > 0) {  // device lattice: (2K + 1)^3 points without the origin (row 0)
+        const int64_t n = 2 * (int64_t)(J.lattice - 1) + 1;
+        if (n > 1023 || n * n * n - 1 >= (int64_t)kMaxRows) {
+          set_error(pre + "image lattice of order " + std::to_string(J.lattice - 1) + " has too many points");
+          return FRIR_ERANGE;
+        }
+        J.n_images = (int32_t)(n * n * n - 1);
+        J.n_images_hi = 0;
+      }
       if (J.n_images < 0 || J.n_images_hi > J.n_images) { set_error(pre + "image count must be >= 0"); return FRIR_EINVAL; }
       if (!(J.duration >= 0) || !(J.reflection >= 0)) {
         set_error(pre + "duration and reflection must be >= 0 (0 = default)");

@@ -184,7 +184,26 @@ __global__ void __launch_bounds__(128, 8) geom_kernel(GeomArgs A) {
   if (g >= ngroups) return;
   const double c_max = __dmul_rn(J.c0, J.t60);
   double th[4], ph[4], dist[4], refl[4];
-  if (A.draw_dist != nullptr) {  // oracle mode: the reference's own ImageSet rows
+  if (ism && J.lattice > 0) {
+    // enumerate_images (ism.py:80-104) on the device: image row i is lattice
+    // point i - 1 of the (2K+1)^3 grid in meshgrid 'ij' order, skipping the
+    // origin (the source, row 0); per axis m L + s (m even) or m L + (L - s)
+    const int K = J.lattice - 1, n = 2 * K + 1, origin = (K * n + K) * n + K;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = min(4 * g + k + 1, I);
+      const int li = (i - 1) < origin ? i - 1 : i;
+      const int m3[3] = {li / (n * n) - K, (li / n) % n - K, li % n - K};
+      double p3[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double L = J.room[a], s = J.center[a], mL = __dmul_rn((double)m3[a], L);
+        p3[a] = (m3[a] & 1) ? __dadd_rn(mL, __dsub_rn(L, s)) : __dadd_rn(mL, s);
+      }
+      dist[k] = p3[0]; th[k] = p3[1]; ph[k] = p3[2];
+      refl[k] = (double)(abs(m3[0]) + abs(m3[1]) + abs(m3[2]));
+    }
+  } else if (A.draw_dist != nullptr) {  // oracle mode: the reference's own ImageSet rows
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       int i = 4 * g + k + 1;

@@ -90,3 +90,17 @@ def test_dropped_arrivals_and_duration():
     ref = P.chain(x, 16000)
     assert out.samples.shape == ref.shape
     assert np.abs(out.samples - ref).max() / np.abs(ref).max() < TOL
+
+
+def test_device_lattice_equals_host_lattice(golden):
+    """The kernel's own lattice enumeration (job field `lattice`) renders the
+    same samples, bit for bit, as the host-enumerated, culled rows."""
+    from paper_2304_08052_b200.ism import ism_batch
+
+    cfgs = [_cfg(golden["ism_meta"][ci]) for ci in (0, 1, 2, 4)]
+    dev = ism_batch(cfgs, device_lattice=True)
+    host = ism_batch(cfgs, device_lattice=False)
+    for a, b in zip(dev, host):
+        assert np.array_equal(a.samples, b.samples)
+        assert np.array_equal(a.direct_path_sample, b.direct_path_sample)
+        assert a.metadata == b.metadata

@@ -178,6 +178,25 @@ def test_jobs_prepare_ism_rules():
         engine.prepare(16000, j, MICS)
 
 
+def test_jobs_prepare_ism_device_lattice():
+    """`lattice` = K + 1: frir_jobs_prepare sizes the job for the (2K+1)^3 - 1
+    lattice points (enumerate_images without the origin, ism.py:80-104)."""
+    j = _one_job()
+    j["kind"] = _abi.KIND_ISM
+    j["d0"] = 0.0
+    for K in (0, 1, 3):
+        j["lattice"] = K + 1
+        pb = engine.prepare(16000, j, MICS)
+        assert pb.jobs[0]["n_images"] == (2 * K + 1) ** 3 - 1
+        assert pb.batch.total_images == (2 * K + 1) ** 3
+    j["lattice"] = -1
+    with pytest.raises(ValueError, match="max_order must be >= 0"):
+        engine.prepare(16000, j, MICS)
+    j["lattice"] = 82  # 163^3 points: past the per-job row limit (2^22)
+    with pytest.raises(_abi.FrirLibraryError, match="too many points"):
+        engine.prepare(16000, j, MICS)
+
+
 def test_header_compiles_as_c_and_links(tmp_path):
     """include/frir.h is plain C (C99): a C program includes it, links
     libfrir.so and calls the host-only entry points."""
