@@ -385,7 +385,30 @@ def run_ours(args):
         "gpu_launches": launches_per_step * K,
         "clocks": sampler.summary(),
     }
+    issue = issue_roofline(cfg, max_render / K, line["clocks"].get("sm_mhz"), dev)
+    if issue:
+        line["roofline"]["issue"] = issue
     return line
+
+
+def issue_roofline(cfg: int, render_ms: float, sm_mhz, dev):
+    """The render kernel is instruction-issue bound: its warp
+    instructions per launch (ncu, committed under profiles/) against the issue
+    slots of the live render time at the sampled SM clock (one warp
+    instruction per cycle per SM sub-partition)."""
+    import torch
+
+    p = ROOT / "profiles" / "r01" / "v6_cfg2_render_ncu_summary.json"
+    if cfg != 2 or not p.exists() or not sm_mhz:
+        return None
+    d = json.loads(p.read_text())[0]
+    inst = float(d["smsp__inst_executed.sum"])
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    slots = render_ms / 1e3 * sm_mhz * 1e6 * sms * 4
+    return {"bound": "issue", "achieved": inst / (render_ms / 1e3) / 1e9, "unit": "G warp-instr/s",
+            "peak": sm_mhz * 1e6 * sms * 4 / 1e9, "frac": inst / slots,
+            "inst_per_launch": inst, "issue_active_pct_ncu": float(d["smsp__issue_active.avg.pct_of_peak_sustained_active"]),
+            "source": str(p.relative_to(ROOT)) + " (ncu --set full, one config-2 render launch)"}
 
 
 def run_e2e(args, batch, early, dev, stream):
