@@ -398,10 +398,12 @@ def issue_roofline(cfg: int, render_ms: float, sm_mhz, dev):
     instruction per cycle per SM sub-partition)."""
     import torch
 
-    p = ROOT / "profiles" / "r01" / "v6_cfg2_render_ncu_summary.json"
+    p = ROOT / "profiles" / "r01" / "v7_cfg2_ncu_full_summary.json"
     if cfg != 2 or not p.exists() or not sm_mhz:
         return None
-    d = json.loads(p.read_text())[0]
+    d = next((r for r in json.loads(p.read_text()) if "render_kernel" in r["Kernel Name"]), None)
+    if d is None:
+        return None
     inst = float(d["smsp__inst_executed.sum"])
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     slots = render_ms / 1e3 * sm_mhz * 1e6 * sms * 4
