@@ -45,6 +45,34 @@ struct Workspace {
   int* counter;
 };
 
+// Segments of long channels (see seg_count); null when the batch has none.
+struct SegWs {
+  int* seg;           // per channel [kSegInts]: segment windows / item ranges (K2 -> K3, K4)
+  double* state;      // per channel [kMaxSeg][F0, F1, E0, E1]: zero-start end states (K3 -> K4)
+  int* units;         // segments >= 1 of long channels as c * kMaxSeg + k (K2 -> K3 work queue)
+  int* nextra;        // entries of units
+};
+
+// Long channels (more than kSegRows items) are rendered as up to kMaxSeg
+// segments of whole tiles by different warps, each from a zero LP state; the
+// seam kernel K4 adds the free response of the true start state afterwards
+// (the LP recursion is linear).  The count depends only on the channel, so a
+// channel renders the same bits in any batch.
+constexpr int kSegRows = 16384, kMaxSeg = 16;
+constexpr int kSegInts = 64;  // [0, S]: first window of each segment; 17 + k: item lo; 33 + k: item hi
+__host__ __device__ inline int seg_count(int rows, int n2) {
+  const int nwin = (n2 + kExt + kWin - 1) / kWin;
+  int s = (rows + kSegRows - 1) / kSegRows;
+  s = s < kMaxSeg ? s : kMaxSeg;
+  const int by_len = nwin / 16 > 1 ? nwin / 16 : 1;  // at least 4 tiles per segment
+  s = s < by_len ? s : by_len;
+  return s > 1 ? s : 1;
+}
+inline int batch_seg_max(const frir_batch* b) {  // upper bound over the batch's channels
+  return seg_count(b->max_rows, b->max_windows * kWin - kExt);
+}
+
+
 __host__ __device__ inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
@@ -58,6 +86,19 @@ Workspace carve(void* base, const frir_batch* b) {
   w.corr = (double*)p; p += align_up((size_t)b->total_channels * 64 * 8);
   w.counter = (int*)p;
   return w;
+}
+
+// The segment tables follow the base workspace (workspace_bytes).
+SegWs carve_seg(void* base, const frir_batch* b) {
+  SegWs g{nullptr, nullptr, nullptr, nullptr};
+  if (batch_seg_max(b) <= 1) return g;
+  char* p = (char*)base + 2 * align_up((size_t)b->total_items * 8) + 2 * align_up((size_t)b->total_channels * 4) +
+            align_up((size_t)b->total_channels * 64 * 8) + 256;
+  g.seg = (int*)p; p += align_up((size_t)b->total_channels * kSegInts * 4);
+  g.state = (double*)p; p += align_up((size_t)b->total_channels * kMaxSeg * 4 * 8);
+  g.units = (int*)p; p += align_up((size_t)b->total_channels * kMaxSeg * 4);
+  g.nextra = (int*)p;
+  return g;
 }
 
 // ---------------------------------------------------------------- K1 geometry + delays
@@ -152,7 +193,10 @@ __device__ __forceinline__ int2 make_item(int q, float a, int r_h, int t0, unsig
   return make_int2((int)(spb | (phi << 20)), __float_as_int(a));
 }
 
-__global__ void __launch_bounds__(128, 8) geom_kernel(GeomArgs A) {
+#ifndef FRIR_GEOM_MINB
+#define FRIR_GEOM_MINB 8
+#endif
+__global__ void __launch_bounds__(128, FRIR_GEOM_MINB) geom_kernel(GeomArgs A) {
   const int j = blockIdx.x;
   const frir_job& J = A.jobs[j];
   const int I = J.n_images, rows = I + 1, M = J.n_mics;
@@ -307,6 +351,7 @@ struct SortArgs {
   const frir_job* jobs;
   const int32_t* chan_job;
   Workspace ws;
+  SegWs sw;
   DevPlan plan;
   int r_h, t0;
 };
@@ -326,7 +371,7 @@ __device__ __forceinline__ void count_add(CT* cnt, int idx) {
     atomicAdd(reinterpret_cast<unsigned*>(cnt) + idx, 1u);
 }
 
-template <typename CT, int NW>  // NW warps per channel (more for long rows)
+template <typename CT, int NW, bool SEG>  // NW warps per channel (more for long rows); SEG: segment tables
 __global__ void __launch_bounds__(NW * 32) sort_kernel(SortArgs A) {
   constexpr int kSortWarps = NW, kSortThreads = NW * 32;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -377,6 +422,45 @@ __global__ void __launch_bounds__(NW * 32) sort_kernel(SortArgs A) {
     run += cnt;
   }
   __syncthreads();
+  const int S = SEG ? seg_count(rows, J.n2) : 1;
+  if (SEG && tid == 0) A.sw.seg[(size_t)c * kSegInts + 63] = S;  // read by K3 / K4
+  if (S > 1) {
+    // segment boundaries of a long channel: whole tiles, about rows / S items
+    // each, every segment at least one tile.  s_cnt[b * NW] is now the number
+    // of items in buckets < b.  Bucket b feeds windows b - 2 .. b - 2 + tbk
+    // (tbk = 32-tap table blocks), so segment k renders windows [W_k, W_k+1)
+    // from the items of buckets [W_k + 2 - tbk, W_k+1 + 1].
+    if (tid == 0) {
+      const int nwin = (J.n2 + kExt + kWin - 1) / kWin;
+      const int top = (nwin / kTileWin) * kTileWin;  // last segment start <= top - kTileWin
+      const int tbk = (A.plan.d.sup + 31) / 32;
+      auto start = [&](int b) { return (int)s_cnt[b * kSortWarps]; };
+      int* seg = A.sw.seg + (size_t)c * kSegInts;
+      int wprev = 0;
+      seg[0] = 0;
+      for (int k = 1; k < S; ++k) {
+        const long long t = (long long)k * rows / S;
+        int lo = 0, hi = nbk - 1;  // smallest b with start(b) >= t
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (start(mid) >= t) hi = mid; else lo = mid + 1;
+        }
+        int wk = ((lo > 1 ? lo - 1 : 0) / kTileWin) * kTileWin;
+        wk = max(wk, wprev + kTileWin);
+        wk = min(wk, top - kTileWin * (S - k));
+        seg[k] = wk;
+        seg[17 + k] = start(wk + 2 - tbk);
+        seg[33 + k - 1] = start(wk + 2);
+        wprev = wk;
+      }
+      seg[S] = nwin;
+      seg[17] = 0;
+      seg[33 + S - 1] = rows;
+      const int at = atomicAdd(A.sw.nextra, S - 1);  // queue order only: outputs do not depend on it
+      for (int k = 1; k < S; ++k) A.sw.units[at + k - 1] = c * kMaxSeg + k;
+    }
+    __syncthreads();  // the scatter below advances s_cnt
+  }
   // pass 2: stable scatter, warp w walks its chunk in row order; early flags
   // (core.py:259-264) from the channel's direct arrival q0
   const int q0 = A.ws.chan_q0[c];
@@ -599,9 +683,11 @@ struct RenderArgs {
   const int32_t* chan_order;
   int total_channels;
   Workspace ws;
+  SegWs sw;
   DevPlan plan;
   float* out_full;
   float* out_early;
+  int seg_max;  // upper bound of seg_count over the batch (work units = seg_max x channels)
 };
 
 __device__ __forceinline__ void sts_f32(unsigned addr, float v) {
@@ -755,9 +841,10 @@ struct Channel {
   }
 };
 
-template <bool EARLY, int NBK>
+template <bool EARLY, int NBK, bool SEG>  // SEG: the batch may hold segmented channels
 __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(const __grid_constant__ RenderArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_stidx[kWarps];
   const frir_plan_desc& d = A.plan.d;
   constexpr int kRow = 64 * NBK;  // doubled rows (see Channel::add)
   constexpr int V = EARLY ? 2 : 1;
@@ -789,16 +876,29 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(const __grid_
   const unsigned down_magic = (unsigned)((0x100000000ull + down - 1) / down);  // exact for e < 2^32 / down
 
   for (;;) {
-    int ci = 0;
-    if (lane == 0) ci = atomicAdd(A.ws.counter, 1);
-    ci = __shfl_sync(0xffffffffu, ci, 0);
-    if (ci >= A.total_channels) break;
-    const int c = A.chan_order ? A.chan_order[ci] : ci;
+    // work unit v: first the later segments of long channels (K2's list, the
+    // longest work), then the first segment of every channel, longest first
+    int v = 0;
+    if (lane == 0) v = atomicAdd(A.ws.counter, 1);
+    v = __shfl_sync(0xffffffffu, v, 0);
+    const int nextra = SEG ? *A.sw.nextra : 0;
+    int c, sg = 0;
+    if (v < nextra) {
+      const int u = A.sw.units[v];
+      c = u / kMaxSeg;
+      sg = u - c * kMaxSeg;
+    } else {
+      const int ci = v - nextra;
+      if (ci >= A.total_channels) break;
+      c = A.chan_order ? A.chan_order[ci] : ci;
+    }
     const int j = A.chan_job[c];
     const frir_job& J = A.jobs[j];
     const int m = c - J.chan_off;
     const int rows = J.n_images + 1;
     const int n1 = J.n1, n2 = J.n2;
+    const int nseg = SEG ? A.sw.seg[(size_t)c * kSegInts + 63] : 1;  // K2's seg_count
+    if (SEG && lane == 0) s_stidx[warp] = nseg > 1 ? c * kMaxSeg + sg : -1;  // end-state slot (flush of the last tile)
     const int nrow = min(J.out_stride, (n2 + 3) & ~3);  // row incl. alignment padding
     const double scale = (double)A.ws.chan_scale[c];
     const int2* items = A.ws.items + J.item_off + (size_t)m * rows;
@@ -818,7 +918,7 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(const __grid_
     // ---- head pre-pass: items whose stage-1 taps reach mid index < 0 (a
     // prefix of the bucket-sorted list; only sources within a few cm of a mic)
     bool head_on = false;  // head corrections pending in head_s
-    for (int p = 0; p < rows; p += 32) {
+    for (int p = 0; sg == 0 && p < rows; p += 32) {
       const int2 mine = p + lane < rows ? items[p + lane] : make_int2(0xFFFFF, 0);
       const int cnt = min(32, rows - p);
       const int qm = r_h * ((mine.x & 0xFFFFF) - kSpBias - kExt) - d.t0 - (((unsigned)mine.x >> 20) & 0x3FF);
@@ -870,13 +970,19 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(const __grid_
     __syncwarp();
 
     // ---- ordered sweep: windows w = -2 .. nwin-1 over n'' = n + kExt
-    const int nwin = (n2 + kExt + kWin - 1) / kWin;
+    // this segment: windows [w_lo, nwin), items [i_lo, i_hi) of the sorted row
+    int w_lo = 0, nwin = (n2 + kExt + kWin - 1) / kWin, i_lo = 0, i_hi = rows;  // this segment
+    if (SEG && nseg > 1) {
+      const int* seg = A.sw.seg + (size_t)c * kSegInts;
+      w_lo = seg[sg]; nwin = seg[sg + 1]; i_lo = seg[17 + sg]; i_hi = seg[33 + sg];
+    }
+
     Channel<EARLY, NBK> ch;
     ch.clear();
     double sF0 = 0.0, sF1 = 0.0, sE0 = 0.0, sE1 = 0.0;
     bool e_dead = false;  // early ring-down negligible: outputs are zeros
     double e_ref = 0.0;   // largest early LP state seen while early items fed tiles
-    int w = -2;           // window held by the front accumulators
+    int w = w_lo - 2;     // window held by the front accumulators
     int slot = -2;        // next tile slot (negative: scratch windows)
     bool est = true;      // the current tile is not quiet: early windows are stored
     auto flush = [&]() {
@@ -929,6 +1035,13 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(const __grid_
             if (n0 + k >= 0 && n0 + k < nrow) outE[n0 + k] = 0.f;
         }
       }
+      if (SEG && w == nwin - 1 && lane == 0) {  // last tile of the sweep: zero-start end state of a segment (K4)
+        const int si = s_stidx[warp];
+        if (si >= 0) {
+          double* st = A.sw.state + (size_t)si * 4;
+          st[0] = sF0; st[1] = sF1; st[2] = sE0; st[3] = sE1;
+        }
+      }
       __syncwarp();
       slot = 0;
       est = w + 1 <= ew_hi;  // the next tile starts at window w + 1
@@ -946,18 +1059,20 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(const __grid_
       ch.shift();
       ++w;
     };
-    int2 nxt = lane < rows ? items[lane] : make_int2(0xFFFFF, 0);  // sentinel: last bucket
-    for (int p = 0; p < rows; p += 32) {
+    const int2* sitems = items + i_lo;  // the segment's items
+    const int srows = i_hi - i_lo;
+    int2 nxt = lane < srows ? sitems[lane] : make_int2(0xFFFFF, 0);  // sentinel: last bucket
+    for (int p = 0; p < srows; p += 32) {
       const int2 mine = nxt;
       const int pn = p + 32 + lane;
-      nxt = pn < rows ? items[pn] : make_int2(0xFFFFF, 0);  // prefetch the next batch
+      nxt = pn < srows ? sitems[pn] : make_int2(0xFFFFF, 0);  // prefetch the next batch
       const int bk = (mine.x & 0xFFFFF) >> 5;
       const unsigned dec = (((unsigned)mine.x >> 20) & 0x3FFu) * (512u * NBK) + 8u * (32u - (mine.x & 31));
-      FRIR_CHECK(p + lane >= rows || (((unsigned)mine.x >> 20) & 0x3FFu) < (unsigned)r_h);
+      FRIR_CHECK(p + lane >= srows || (((unsigned)mine.x >> 20) & 0x3FFu) < (unsigned)r_h);
       __syncwarp();
       s_it[lane] = make_int2((int)dec, mine.y);
       __syncwarp();
-      const int cnt = min(32, rows - p);
+      const int cnt = min(32, srows - p);
       const unsigned emask = EARLY ? __ballot_sync(0xffffffffu, lane < cnt && mine.y < 0) : 0u;
       int jj = 0;
       while (jj < cnt) {  // runs of equal bucket (items are bucket-sorted)
@@ -984,6 +1099,79 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(const __grid_
   }
 }
 
+// ---------------------------------------------------------------- K4 segment seams
+// A long channel's segments were rendered from zero LP state (K3).  With the
+// LP recursion linear, the true output of segment k is the zero-start output
+// minus the free response of its true start state t_k, and
+// t_k = e_(k-1) + M^len(k-1) t_(k-1) (e = zero-start end state, M^len by
+// squaring M^kTile).  One warp per channel applies -scale * LPfree to the
+// segment's tiles until the response is below 2^-44 of t_k.  (The response
+// is at most the size of the low-pass branch, so the FP32 rounding of the
+// zero-start output costs ~1 ulp of the channel's peak.)
+struct SeamArgs {
+  const frir_job* jobs;
+  const int32_t* chan_job;
+  Workspace ws;
+  SegWs sw;
+  DevPlan plan;
+  float* out_full;
+  float* out_early;
+  int total_channels;
+};
+
+__global__ void __launch_bounds__(256) seam_kernel(const __grid_constant__ SeamArgs A) {
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (c >= A.total_channels) return;
+  const frir_job& J = A.jobs[A.chan_job[c]];
+  const int n2 = J.n2;
+  const int nseg = seg_count(J.n_images + 1, n2);
+  if (nseg == 1) return;
+  const int m = c - J.chan_off;
+  const double scale = (double)A.ws.chan_scale[c];
+  const int* seg = A.sw.seg + (size_t)c * kSegInts;
+  const double* est = A.sw.state + (size_t)c * kMaxSeg * 4;
+  const double* Mt = A.plan.mt;
+  const double* fr = A.plan.scan + kScanFree + 2 * kChunk * lane;
+  double f[2 * kChunk];
+#pragma unroll
+  for (int k = 0; k < 2 * kChunk; ++k) f[k] = fr[k];
+  const int V = A.out_early ? 2 : 1;
+  for (int v = 0; v < V; ++v) {
+    float* out = (v ? A.out_early : A.out_full) + J.out_off + (size_t)m * J.out_stride;
+    double t0 = 0.0, t1 = 0.0;  // true start state of segment k
+    for (int k = 1; k < nseg; ++k) {
+      double x0 = t0, x1 = t1;  // M^(kTile * tiles) t
+      double p0 = Mt[0], p1 = Mt[1], p2 = Mt[2], p3 = Mt[3];
+      for (int e = (seg[k] - seg[k - 1]) / kTileWin; e; e >>= 1) {
+        if (e & 1) {
+          const double y0 = fma(p0, x0, p1 * x1), y1 = fma(p2, x0, p3 * x1);
+          x0 = y0; x1 = y1;
+        }
+        const double q0 = fma(p0, p0, p1 * p2), q1 = fma(p0, p1, p1 * p3);
+        const double q2 = fma(p2, p0, p3 * p2), q3 = fma(p2, p1, p3 * p3);
+        p0 = q0; p1 = q1; p2 = q2; p3 = q3;
+      }
+      t0 = est[4 * (k - 1) + 2 * v] + x0;
+      t1 = est[4 * (k - 1) + 2 * v + 1] + x1;
+      double s0 = t0, s1 = t1;
+      const double cut = 0x1p-44 * (fabs(t0) + fabs(t1));
+      for (int tw = seg[k]; tw < seg[k + 1]; tw += kTileWin) {
+        if (!(fabs(s0) + fabs(s1) > cut)) break;  // warp-uniform
+        const int n0 = tw * kWin - kExt + kChunk * lane;
+#pragma unroll
+        for (int kk = 0; kk < kChunk; ++kk) {
+          const int n = n0 + kk;
+          if (n >= 0 && n < n2)
+            out[n] = (float)((double)out[n] - scale * fma(f[2 * kk], s0, f[2 * kk + 1] * s1));
+        }
+        const double y0 = fma(Mt[0], s0, Mt[1] * s1), y1 = fma(Mt[2], s0, Mt[3] * s1);
+        s0 = y0; s1 = y1;
+      }
+    }
+  }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- host launcher
@@ -994,8 +1182,13 @@ int check_line() {
 }
 
 size_t workspace_bytes(const frir_batch* b) {
-  return 2 * align_up((size_t)b->total_items * 8) + 2 * align_up((size_t)b->total_channels * 4) +
-         align_up((size_t)b->total_channels * 64 * 8) + 256;
+  size_t n = 2 * align_up((size_t)b->total_items * 8) + 2 * align_up((size_t)b->total_channels * 4) +
+             align_up((size_t)b->total_channels * 64 * 8) + 256;
+  const int smax = batch_seg_max(b);
+  if (smax > 1)
+    n += align_up((size_t)b->total_channels * kSegInts * 4) + align_up((size_t)b->total_channels * kMaxSeg * 4 * 8) +
+         align_up((size_t)b->total_channels * kMaxSeg * 4) + 256;
+  return n;
 }
 
 static int table_blocks(const frir_plan_desc& d) { return (d.sup + 31) / 32; }
@@ -1007,28 +1200,29 @@ static size_t render_smem(const frir_plan_desc& d, bool early) {
          (size_t)kWarps * v * 2 * 64 * 4;
 }
 
-template <bool EARLY, int NBK>
+template <bool EARLY, int NBK, bool SEG>
 static cudaError_t launch_render(const RenderArgs& ra, const frir_plan_desc& d, long channels,
                                  cudaStream_t st) {
   size_t smem = render_smem(d, EARLY);
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaError_t e = cudaFuncSetAttribute(render_kernel<EARLY, NBK>,
+  cudaError_t e = cudaFuncSetAttribute(render_kernel<EARLY, NBK, SEG>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, render_kernel<EARLY, NBK>, kRenderThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, render_kernel<EARLY, NBK, SEG>, kRenderThreads, smem);
   if (per_sm < 1) per_sm = 1;
-  long want = (channels + kWarps - 1) / kWarps;
+  long want = (channels * ra.seg_max + kWarps - 1) / kWarps;  // upper bound of the work units
   int grid = (int)std::min<long>((long)sms * per_sm, want);
-  render_kernel<EARLY, NBK><<<grid, kRenderThreads, smem, st>>>(ra);
+  render_kernel<EARLY, NBK, SEG><<<grid, kRenderThreads, smem, st>>>(ra);
   return cudaGetLastError();
 }
 
 int launches(const frir_batch* b, int early) {
-  (void)b;
   (void)early;
-  return 4;  // geom, sort, tail, render (plus one memset of the work counter)
+  // geom, sort, tail, render (plus one memset of the work counter); the seam
+  // kernel when the batch may hold segmented (long) channels
+  return 4 + (batch_seg_max(b) > 1 ? 1 : 0);
 }
 
 int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_t ws_bytes,
@@ -1046,6 +1240,7 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_
   }
   if (b->n_jobs == 0 || b->total_channels == 0) return FRIR_OK;
   Workspace ws = carve(wsp, b);
+  const SegWs sw = carve_seg(wsp, b);
   cudaError_t e = cudaSuccess;
 
   const int rate = d.r_h * d.sample_rate;
@@ -1066,15 +1261,21 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_
 
   if (stages & FRIR_STAGE_DELAY) {  // K2: early flags + stable bucket sort per channel
     SortArgs sa;
-    sa.jobs = b->jobs; sa.chan_job = b->chan_job; sa.ws = ws;
+    sa.jobs = b->jobs; sa.chan_job = b->chan_job; sa.ws = ws; sa.sw = sw;
     sa.r_h = d.r_h; sa.t0 = d.t0; sa.plan = plan->dev;
     const int nbk = ((b->max_windows * kWin + kSpBias) >> 5) + 3;
+    if (sw.nextra) {
+      e = cudaMemsetAsync(sw.nextra, 0, sizeof(int), st);
+      if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FRIR_ECUDA; }
+    }
     const bool wide = b->max_rows > 65535;  // sorted positions need 32-bit counters
     const bool big = b->total_items >= 4096LL * b->total_channels;  // long rows on average: 16 warps
     const int nw = big ? 16 : 8;
     const size_t smem = align16((size_t)nbk * nw * (wide ? 4 : 2));
-    auto kern = wide ? (big ? sort_kernel<uint32_t, 16> : sort_kernel<uint32_t, 8>)
-                     : (big ? sort_kernel<uint16_t, 16> : sort_kernel<uint16_t, 8>);
+    auto kern = sw.seg ? (wide ? (big ? sort_kernel<uint32_t, 16, true> : sort_kernel<uint32_t, 8, true>)
+                               : (big ? sort_kernel<uint16_t, 16, true> : sort_kernel<uint16_t, 8, true>))
+                       : (wide ? (big ? sort_kernel<uint32_t, 16, false> : sort_kernel<uint32_t, 8, false>)
+                               : (big ? sort_kernel<uint16_t, 16, false> : sort_kernel<uint16_t, 8, false>));
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess) {
       kern<<<b->total_channels, nw * 32, smem, st>>>(sa);
@@ -1098,15 +1299,31 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_
   if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FRIR_ECUDA; }
   RenderArgs ra;
   ra.jobs = b->jobs; ra.chan_job = b->chan_job; ra.chan_order = b->chan_order;
-  ra.total_channels = b->total_channels; ra.ws = ws; ra.plan = plan->dev;
+  ra.total_channels = b->total_channels; ra.ws = ws; ra.sw = sw; ra.plan = plan->dev;
   ra.out_full = out_full; ra.out_early = out_early;
+  ra.seg_max = batch_seg_max(b);
   const bool early = out_early != nullptr;
   const int nbk = table_blocks(d);
-  if (nbk == 1) e = early ? launch_render<true, 1>(ra, d, b->total_channels, st)
-                          : launch_render<false, 1>(ra, d, b->total_channels, st);
-  else e = early ? launch_render<true, 2>(ra, d, b->total_channels, st)
-                 : launch_render<false, 2>(ra, d, b->total_channels, st);
+  const bool seg = ra.seg_max > 1;
+  if (nbk == 1)
+    e = early ? (seg ? launch_render<true, 1, true>(ra, d, b->total_channels, st)
+                     : launch_render<true, 1, false>(ra, d, b->total_channels, st))
+              : (seg ? launch_render<false, 1, true>(ra, d, b->total_channels, st)
+                     : launch_render<false, 1, false>(ra, d, b->total_channels, st));
+  else
+    e = early ? (seg ? launch_render<true, 2, true>(ra, d, b->total_channels, st)
+                     : launch_render<true, 2, false>(ra, d, b->total_channels, st))
+              : (seg ? launch_render<false, 2, true>(ra, d, b->total_channels, st)
+                     : launch_render<false, 2, false>(ra, d, b->total_channels, st));
   if (e != cudaSuccess) { set_error(std::string("render_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
+  if (ra.seg_max > 1) {  // K4: seams of segmented channels
+    SeamArgs sa;
+    sa.jobs = b->jobs; sa.chan_job = b->chan_job; sa.ws = ws; sa.sw = sw; sa.plan = plan->dev;
+    sa.out_full = out_full; sa.out_early = out_early; sa.total_channels = b->total_channels;
+    seam_kernel<<<(b->total_channels + 7) / 8, 256, 0, st>>>(sa);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) { set_error(std::string("seam_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
+  }
   }
   return FRIR_OK;
 }
