@@ -40,6 +40,7 @@ struct Workspace {
   int2* items;      // per channel, sorted by output window (K2 -> K3)
   int2* items_raw;  // per channel, image order (K1 -> K2)
   int* chan_q0;
+  int* chan_rows;   // items per channel before the dropped-arrival bucket (K2 -> K2b, K3)
   float* chan_scale;
   double* corr;     // per channel [F, E][32]: tail corrections of outputs n_c + i (K2 -> K3)
   int* counter;
@@ -82,6 +83,7 @@ Workspace carve(void* base, const frir_batch* b) {
   w.items = (int2*)p; p += align_up((size_t)b->total_items * 8);
   w.items_raw = (int2*)p; p += align_up((size_t)b->total_items * 8);
   w.chan_q0 = (int*)p; p += align_up((size_t)b->total_channels * 4);
+  w.chan_rows = (int*)p; p += align_up((size_t)b->total_channels * 4);
   w.chan_scale = (float*)p; p += align_up((size_t)b->total_channels * 4);
   w.corr = (double*)p; p += align_up((size_t)b->total_channels * 64 * 8);
   w.counter = (int*)p;
@@ -92,7 +94,7 @@ Workspace carve(void* base, const frir_batch* b) {
 SegWs carve_seg(void* base, const frir_batch* b) {
   SegWs g{nullptr, nullptr, nullptr, nullptr};
   if (batch_seg_max(b) <= 1) return g;
-  char* p = (char*)base + 2 * align_up((size_t)b->total_items * 8) + 2 * align_up((size_t)b->total_channels * 4) +
+  char* p = (char*)base + 2 * align_up((size_t)b->total_items * 8) + 3 * align_up((size_t)b->total_channels * 4) +
             align_up((size_t)b->total_channels * 64 * 8) + 256;
   g.seg = (int*)p; p += align_up((size_t)b->total_channels * kSegInts * 4);
   g.state = (double*)p; p += align_up((size_t)b->total_channels * kMaxSeg * 4 * 8);
@@ -196,6 +198,13 @@ __device__ __forceinline__ int2 make_item(int q, float a, int r_h, int t0, unsig
 #ifndef FRIR_GEOM_MINB
 #define FRIR_GEOM_MINB 8
 #endif
+// Buckets of a channel's items (32-sample output windows, biased) and the
+// extra bucket after them that holds ISM arrivals past the train end
+// (ism.py:131-133 drops them): the sort puts them last and K2b / K3 stop
+// before them.
+__host__ __device__ inline int legit_buckets(int n2) { return ((n2 + kExt + kSpBias) >> 5) + 2; }
+__device__ __forceinline__ int2 dropped_item(int n2) { return make_int2(legit_buckets(n2) << 5, 0); }
+
 __global__ void __launch_bounds__(128, FRIR_GEOM_MINB) geom_kernel(GeomArgs A) {
   const int j = blockIdx.x;
   const frir_job& J = A.jobs[j];
@@ -212,12 +221,11 @@ __global__ void __launch_bounds__(128, FRIR_GEOM_MINB) geom_kernel(GeomArgs A) {
     for (int m = 0; m < M; ++m) {
       double D;
       int q = delay_of(x, y, z, mics + 3 * m, J.c0, A.rate, rate_c0, J.L + ism, &D);
-      // ISM drops arrivals past the train end (ism.py:131-133): gain 0 at a
-      // neutral mid-train position; the direct index still clamps (:134-136)
+      // ISM drops arrivals past the train end (ism.py:131-133): they go to the
+      // dropped-arrival bucket; the direct index still clamps (:134-136)
       const bool drop = q > J.L - 1;
       q = min(q, J.L - 1);
-      items[(size_t)m * rows] = make_item(drop ? J.L / 2 : q, drop ? 0.f : (float)__drcp_rn(D), A.r_h, A.t0,
-                                          A.rh_magic);
+      items[(size_t)m * rows] = drop ? dropped_item(J.n2) : make_item(q, (float)__drcp_rn(D), A.r_h, A.t0, A.rh_magic);
       A.ws.chan_q0[J.chan_off + m] = q;
       A.ws.chan_scale[J.chan_off + m] = J.normalize ? (float)D : 1.0f;  // direct path -> 1/(1 m)
       // resample.py:115-119: clip(round(q0 / r_h), 0, n2 - 1), half-even
@@ -319,7 +327,7 @@ __global__ void __launch_bounds__(128, FRIR_GEOM_MINB) geom_kernel(GeomArgs A) {
         float inv_d;
         const int q = delay_fast(px[k], py[k], pz[k], mx, my, mz, J.c0, A.rate, rate_c0, J.L + ism, &inv_d);
         if (q > J.L - 1) {  // ISM only: dropped arrival
-          out[k] = make_item(J.L / 2, 0.f, A.r_h, A.t0, A.rh_magic);
+          out[k] = dropped_item(J.n2);
           continue;
         }
         FRIR_CHECK(q >= 0 && q < J.L && r0 + k < rows);
@@ -381,7 +389,7 @@ __global__ void __launch_bounds__(NW * 32) sort_kernel(SortArgs A) {
   const frir_job& J = A.jobs[j];
   const int m = c - J.chan_off;
   const int rows = J.n_images + 1;
-  const int nbk = ((J.n2 + kExt + kSpBias) >> 5) + 2;  // buckets 0 .. nbk-1
+  const int nbk = legit_buckets(J.n2) + 1;  // buckets 0 .. nbk-1, the last one for dropped arrivals
   const size_t base = J.item_off + (size_t)m * rows;
   const int2* src = A.ws.items_raw + base;
   int2* dst = A.ws.items + base;
@@ -422,7 +430,9 @@ __global__ void __launch_bounds__(NW * 32) sort_kernel(SortArgs A) {
     run += cnt;
   }
   __syncthreads();
-  const int S = SEG ? seg_count(rows, J.n2) : 1;
+  const int nvalid = (int)s_cnt[(nbk - 1) * kSortWarps];  // items before the dropped-arrival bucket
+  if (tid == 0) A.ws.chan_rows[c] = nvalid;
+  const int S = SEG ? seg_count(nvalid, J.n2) : 1;
   if (SEG && tid == 0) A.sw.seg[(size_t)c * kSegInts + 63] = S;  // read by K3 / K4
   if (S > 1) {
     // segment boundaries of a long channel: whole tiles, about rows / S items
@@ -439,7 +449,7 @@ __global__ void __launch_bounds__(NW * 32) sort_kernel(SortArgs A) {
       int wprev = 0;
       seg[0] = 0;
       for (int k = 1; k < S; ++k) {
-        const long long t = (long long)k * rows / S;
+        const long long t = (long long)k * nvalid / S;
         int lo = 0, hi = nbk - 1;  // smallest b with start(b) >= t
         while (lo < hi) {
           const int mid = (lo + hi) >> 1;
@@ -455,7 +465,7 @@ __global__ void __launch_bounds__(NW * 32) sort_kernel(SortArgs A) {
       }
       seg[S] = nwin;
       seg[17] = 0;
-      seg[33 + S - 1] = rows;
+      seg[33 + S - 1] = nvalid;
       const int at = atomicAdd(A.sw.nextra, S - 1);  // queue order only: outputs do not depend on it
       for (int k = 1; k < S; ++k) A.sw.units[at + k - 1] = c * kMaxSeg + k;
     }
@@ -535,9 +545,9 @@ __global__ void __launch_bounds__(kTailThreads) tail_kernel(const __grid_constan
   const int j = A.chan_job[c];
   const frir_job& J = A.jobs[j];
   const int m = c - J.chan_off;
-  const int rows = J.n_images + 1;
+  const int2* items = A.ws.items + J.item_off + (size_t)m * (J.n_images + 1);
+  const int rows = A.ws.chan_rows[c];  // sorted items before the dropped-arrival bucket
   const int n1 = J.n1, n2 = J.n2;
-  const int2* items = A.ws.items + J.item_off + (size_t)m * rows;
   const int up = d.up, down = d.down, half1 = d.half1, r_h = d.r_h;
   const unsigned down_magic = (unsigned)((0x100000000ull + down - 1) / down);  // exact for e < 2^32 / down
   const int kthr = n1 - d.horizon;  // items with k_hi >= kthr feed the state
@@ -902,6 +912,7 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(const __grid_
     const int nrow = min(J.out_stride, (n2 + 3) & ~3);  // row incl. alignment padding
     const double scale = (double)A.ws.chan_scale[c];
     const int2* items = A.ws.items + J.item_off + (size_t)m * rows;
+    const int nvalid = A.ws.chan_rows[c];  // sorted items before the dropped-arrival bucket
     float* outF = A.out_full + J.out_off + (size_t)m * J.out_stride;
     float* outE = EARLY ? A.out_early + J.out_off + (size_t)m * J.out_stride : nullptr;
 
@@ -918,9 +929,9 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(const __grid_
     // ---- head pre-pass: items whose stage-1 taps reach mid index < 0 (a
     // prefix of the bucket-sorted list; only sources within a few cm of a mic)
     bool head_on = false;  // head corrections pending in head_s
-    for (int p = 0; sg == 0 && p < rows; p += 32) {
-      const int2 mine = p + lane < rows ? items[p + lane] : make_int2(0xFFFFF, 0);
-      const int cnt = min(32, rows - p);
+    for (int p = 0; sg == 0 && p < nvalid; p += 32) {
+      const int2 mine = p + lane < nvalid ? items[p + lane] : make_int2(0xFFFFF, 0);
+      const int cnt = min(32, nvalid - p);
       const int qm = r_h * ((mine.x & 0xFFFFF) - kSpBias - kExt) - d.t0 - (((unsigned)mine.x >> 20) & 0x3FF);
       unsigned hm = __ballot_sync(0xffffffffu, lane < cnt && up * qm < half1);
       if (hm) {
@@ -971,7 +982,7 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(const __grid_
 
     // ---- ordered sweep: windows w = -2 .. nwin-1 over n'' = n + kExt
     // this segment: windows [w_lo, nwin), items [i_lo, i_hi) of the sorted row
-    int w_lo = 0, nwin = (n2 + kExt + kWin - 1) / kWin, i_lo = 0, i_hi = rows;  // this segment
+    int w_lo = 0, nwin = (n2 + kExt + kWin - 1) / kWin, i_lo = 0, i_hi = nvalid;  // this segment
     if (SEG && nseg > 1) {
       const int* seg = A.sw.seg + (size_t)c * kSegInts;
       w_lo = seg[sg]; nwin = seg[sg + 1]; i_lo = seg[17 + sg]; i_hi = seg[33 + sg];
@@ -1125,7 +1136,7 @@ __global__ void __launch_bounds__(256) seam_kernel(const __grid_constant__ SeamA
   if (c >= A.total_channels) return;
   const frir_job& J = A.jobs[A.chan_job[c]];
   const int n2 = J.n2;
-  const int nseg = seg_count(J.n_images + 1, n2);
+  const int nseg = A.sw.seg[(size_t)c * kSegInts + 63];  // K2's seg_count
   if (nseg == 1) return;
   const int m = c - J.chan_off;
   const double scale = (double)A.ws.chan_scale[c];
@@ -1182,7 +1193,7 @@ int check_line() {
 }
 
 size_t workspace_bytes(const frir_batch* b) {
-  size_t n = 2 * align_up((size_t)b->total_items * 8) + 2 * align_up((size_t)b->total_channels * 4) +
+  size_t n = 2 * align_up((size_t)b->total_items * 8) + 3 * align_up((size_t)b->total_channels * 4) +
              align_up((size_t)b->total_channels * 64 * 8) + 256;
   const int smax = batch_seg_max(b);
   if (smax > 1)
