@@ -513,11 +513,14 @@ __global__ void __launch_bounds__(NW * 32) sort_kernel(SortArgs A) {
 // the HP state at n1 (a modal sum over the items within the HP horizon, a
 // suffix of the sorted row) and on the stage-1 taps the items put past n1.
 // One warp per channel; the small power tables live in smem.  Every sum runs
-// in a fixed order, so the corrections are bit-reproducible.
+// in a fixed order, so the corrections are bit-reproducible.  Segmented
+// (long) channels are left to the SPLIT instance, where the CTA's warps take
+// contiguous parts of the suffix and warp 0 adds their sums in warp order.
 struct TailArgs {
   const frir_job* jobs;
   const int32_t* chan_job;
   Workspace ws;
+  SegWs sw;
   DevPlan plan;
   int total_channels;
 };
@@ -525,6 +528,7 @@ struct TailArgs {
 constexpr int kTailThreads = 128;
 constexpr int kTailWarps = kTailThreads / 32;
 
+template <bool SPLIT>
 __global__ void __launch_bounds__(kTailThreads) tail_kernel(const __grid_constant__ TailArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const DevPlan& P = A.plan;
@@ -540,8 +544,10 @@ __global__ void __launch_bounds__(kTailThreads) tail_kernel(const __grid_constan
   for (int i = threadIdx.x; i < nphi; i += blockDim.x) s_phi[i] = make_double2(P.ppow_hi[2 * i], P.ppow_hi[2 * i + 1]);
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int c = blockIdx.x * kTailWarps + warp;
+  const int c = SPLIT ? blockIdx.x : blockIdx.x * kTailWarps + warp;
   if (c >= A.total_channels) return;
+  const bool long_chan = A.sw.seg != nullptr && A.sw.seg[(size_t)c * kSegInts + 63] > 1;
+  if (long_chan != SPLIT) return;  // (CTA-uniform when SPLIT)
   const int j = A.chan_job[c];
   const frir_job& J = A.jobs[j];
   const int m = c - J.chan_off;
@@ -574,21 +580,27 @@ __global__ void __launch_bounds__(kTailThreads) tail_kernel(const __grid_constan
     }
     p_t = max(p_t, 0);
   }
+  int p_hi = rows;  // this warp's part of the suffix [p_t, p_hi)
+  if (SPLIT) {
+    const int chunk = ((rows - p_t + 32 * kTailWarps - 1) / (32 * kTailWarps)) * 32;
+    p_t = min(rows, p_t + warp * chunk);
+    p_hi = min(rows, p_t + chunk);
+  }
   double4 z = make_double4(0.0, 0.0, 0.0, 0.0);  // this lane's partial modal sums (F, E)
   constexpr int kGroup = 8;  // batches loaded together (memory-level parallelism)
-  for (int p0 = p_t; p0 < rows; p0 += 32 * kGroup) {
+  for (int p0 = p_t; p0 < p_hi; p0 += 32 * kGroup) {
   int2 grp[kGroup];
 #pragma unroll
   for (int u = 0; u < kGroup; ++u) {
     const int idx = p0 + 32 * u + lane;
-    grp[u] = idx < rows ? items[idx] : make_int2(0xFFFFF, 0);
+    grp[u] = idx < p_hi ? items[idx] : make_int2(0xFFFFF, 0);
   }
 #pragma unroll
   for (int u = 0; u < kGroup; ++u) {
     const int p = p0 + 32 * u;
-    if (p >= rows) break;
+    if (p >= p_hi) break;
     const int2 it = grp[u];
-    const int cnt = min(32, rows - p);
+    const int cnt = min(32, p_hi - p);
     const int spb = it.x & 0xFFFFF;
     const int qm = r_h * (spb - kSpBias - kExt) - d.t0 - (((unsigned)it.x >> 20) & 0x3FF);
     const int e = up * qm + half1;  // >= 0
@@ -663,6 +675,19 @@ __global__ void __launch_bounds__(kTailThreads) tail_kernel(const __grid_constan
     zE.im += __shfl_xor_sync(0xffffffffu, zE.im, o);
   }
   __syncwarp();
+  if (SPLIT) {  // warp 0 adds the warps' sums and xt rows in warp order
+    __shared__ double s_z[kTailWarps][4];
+    if (lane == 0) {
+      s_z[warp][0] = zF.re; s_z[warp][1] = zF.im; s_z[warp][2] = zE.re; s_z[warp][3] = zE.im;
+    }
+    __syncthreads();
+    if (warp != 0) return;
+    for (int w2 = 1; w2 < kTailWarps; ++w2) {
+      zF.re += s_z[w2][0]; zF.im += s_z[w2][1]; zE.re += s_z[w2][2]; zE.im += s_z[w2][3];
+      for (int i = lane; i < 2 * ltc; i += 32) xt_s[i] += s_xt[2 * ltc * w2 + i];
+    }
+    __syncwarp();
+  }
   const Cplx v0a = {P.lp[2], P.lp[3]}, v0b = {P.lp[4], P.lp[5]};
   const Cplx ta = cmul(v0a, zF), tb = cmul(v0b, zF), ea = cmul(v0a, zE), eb = cmul(v0b, zE);
   const double s0 = 2.0 * ta.re, s1 = 2.0 * tb.re, se0 = 2.0 * ea.re, se1 = 2.0 * eb.re;
@@ -1231,9 +1256,9 @@ static cudaError_t launch_render(const RenderArgs& ra, const frir_plan_desc& d, 
 
 int launches(const frir_batch* b, int early) {
   (void)early;
-  // geom, sort, tail, render (plus one memset of the work counter); the seam
-  // kernel when the batch may hold segmented (long) channels
-  return 4 + (batch_seg_max(b) > 1 ? 1 : 0);
+  // geom, sort, tail, render (plus one memset of the work counter); the split
+  // tail and the seam kernel when the batch may hold segmented (long) channels
+  return 4 + (batch_seg_max(b) > 1 ? 2 : 0);
 }
 
 int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_t ws_bytes,
@@ -1294,12 +1319,14 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_
     }
     if (e != cudaSuccess) { set_error(std::string("sort_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
     TailArgs ta;  // K2b: tail corrections from the sorted rows
-    ta.jobs = b->jobs; ta.chan_job = b->chan_job; ta.ws = ws; ta.plan = plan->dev;
+    ta.jobs = b->jobs; ta.chan_job = b->chan_job; ta.ws = ws; ta.sw = sw; ta.plan = plan->dev;
     ta.total_channels = b->total_channels;
     const size_t tsm = tail_smem(d);
-    e = cudaFuncSetAttribute(tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+    e = cudaFuncSetAttribute(tail_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+    if (e == cudaSuccess && sw.seg) e = cudaFuncSetAttribute(tail_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
     if (e == cudaSuccess) {
-      tail_kernel<<<(b->total_channels + kTailWarps - 1) / kTailWarps, kTailThreads, tsm, st>>>(ta);
+      tail_kernel<false><<<(b->total_channels + kTailWarps - 1) / kTailWarps, kTailThreads, tsm, st>>>(ta);
+      if (sw.seg) tail_kernel<true><<<b->total_channels, kTailThreads, tsm, st>>>(ta);  // long channels
       e = cudaGetLastError();
     }
     if (e != cudaSuccess) { set_error(std::string("tail_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
