@@ -398,7 +398,7 @@ def issue_roofline(cfg: int, render_ms: float, sm_mhz, dev):
     instruction per cycle per SM sub-partition)."""
     import torch
 
-    p = ROOT / "profiles" / "r01" / "v7_cfg2_ncu_full_summary.json"
+    p = ROOT / "profiles" / "r01" / "v8_cfg2_ncu_full_summary.json"
     if cfg != 2 or not p.exists() or not sm_mhz:
         return None
     d = next((r for r in json.loads(p.read_text()) if "render_kernel" in r["Kernel Name"]), None)
