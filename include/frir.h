@@ -195,7 +195,8 @@ int frir_simulate(const frir_plan* plan, const frir_batch* batch, void* workspac
                   int32_t* direct_index, void* stream);
 
 /* frir_simulate split into its stages (bit 0: sampling/geometry K1, bit 1:
-   delays + per-channel sort K2, bit 2: render K3); stages must run in order on
+   delays + per-channel sort K2 and tail corrections K2b, bit 2: render K3 and,
+   for batches with long channels, the segment seams K4); stages must run in order on
    one stream with the same workspace.  Lets callers time the render kernel. */
 #define FRIR_STAGE_GEOM 1
 #define FRIR_STAGE_DELAY 2

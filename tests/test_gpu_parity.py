@@ -422,3 +422,20 @@ def test_segmented_channels_batch_invariant_and_reproducible():
         assert torch.equal(a.job_view(j), short.job_view(k))
     only = engine.simulate_jobs(16000, jobs_l, mics, include_early=False)
     assert torch.equal(only.job_view(0), alone.job_view(0))
+
+
+def test_segmented_channels_normalize_scales_seams():
+    """normalize=1 scales every output of a channel by its direct distance,
+    across the seams too (K4 applies the same scale to the free response)."""
+    jobs, mics, _ = _long_job(40000, 0.5, 16000, seed=8)
+    plain = engine.simulate_jobs(16000, jobs, mics)
+    jobs_n = jobs.copy()
+    jobs_n["normalize"] = 1
+    norm = engine.simulate_jobs(16000, jobs_n, mics)
+    for var in ("full", "early"):
+        a = plain.job_view(0, var).cpu().numpy().astype(np.float64)
+        b = norm.job_view(0, var).cpu().numpy().astype(np.float64)
+        for m in range(3):
+            s = float(a[m] @ b[m]) / float(a[m] @ a[m])
+            assert s > 0.1
+            assert np.abs(b[m] - s * a[m]).max() <= 1e-6 * np.abs(b[m]).max(), (var, m)
