@@ -297,3 +297,124 @@ class HostPipeline:
         self.copy.synchronize()
         self.compute.synchronize()
         return done
+
+
+def split_jobs(jobs: np.ndarray, mics: np.ndarray, lo: int, hi: int):
+    """Jobs [lo, hi) with only the mic rows they reference (mic_off rebased)."""
+    part = np.array(jobs[lo:hi], copy=True)
+    if len(part) == 0:
+        return part, mics[:0]
+    m0 = int(part["mic_off"].min())
+    m1 = int((part["mic_off"] + part["n_mics"]).max())
+    part["mic_off"] -= m0
+    return part, np.ascontiguousarray(mics[m0:m1])
+
+
+class HostStream:
+    """Bounded-memory end-to-end generation of a large job table.
+
+    The table is cut into parts of ``part_jobs`` jobs.  Every ``run()``
+    validates each part on the host (``frir_jobs_prepare``), copies its job
+    tables host->device from pinned memory, renders it on a compute stream and
+    copies every RIR device->host into one of ``slots`` pinned host slots on a
+    copy stream, so the copy of part k overlaps the render of part k+1.
+    Before a slot is reused, ``consumer(part_index, host)`` (if given) sees the
+    finished part (``host["full"]``, ``host["early"]``, ``host["direct"]`` flat
+    arrays laid out as ``parts[i].jobs`` says).  This is the form a dataloader
+    that keeps RIRs on the host uses for workloads larger than host or device
+    memory (BASELINE config 5: 65,536 32-channel rooms, 109 GB per pass).
+    """
+
+    def __init__(self, sample_rate: int, jobs: np.ndarray, mics: np.ndarray, part_jobs: int = 1024,
+                 include_early: bool = True, slots: int = 2, device=None):
+        require_cuda()
+        self.sample_rate = int(sample_rate)
+        self.include_early = include_early
+        self.dev = torch.device("cuda", torch.cuda.current_device() if device is None
+                                else torch.device(device).index)
+        n = len(jobs)
+        part_jobs = max(1, int(part_jobs))
+        self.src = [split_jobs(jobs, mics, lo, min(n, lo + part_jobs)) for lo in range(0, n, part_jobs)]
+        self.parts = [prepare(self.sample_rate, j, m) for j, m in self.src]
+        self.dbs = [DeviceBatch(p, device=self.dev, workspace=False) for p in self.parts]
+        max_out = max(int(p.batch.total_out) for p in self.parts)
+        max_ch = max(int(p.batch.total_channels) for p in self.parts)
+        max_ws = max(db.workspace_bytes for db in self.dbs)
+        max_jobs = max(p.jobs.nbytes for p in self.parts)
+        max_mics = max(p.mics.size for p in self.parts)
+        max_chj = max(len(p.chan_job) for p in self.parts)
+        self.slots = []
+        for _ in range(max(1, min(slots, len(self.parts)))):
+            self.slots.append({
+                "ws": torch.empty(max_ws, dtype=torch.uint8, device=self.dev),
+                "d_full": torch.empty(max_out, dtype=torch.float32, device=self.dev),
+                "d_early": torch.empty(max_out, dtype=torch.float32, device=self.dev) if include_early else None,
+                "d_direct": torch.empty(max_ch, dtype=torch.int32, device=self.dev),
+                "jobs": torch.empty(max_jobs, dtype=torch.uint8).pin_memory(),
+                "chan_job": torch.empty(max_chj, dtype=torch.int32).pin_memory(),
+                "chan_order": torch.empty(max_chj, dtype=torch.int32).pin_memory(),
+                "mics": torch.empty(max_mics, dtype=torch.float64).pin_memory(),
+                "full": torch.empty(max_out, dtype=torch.float32).pin_memory(),
+                "early": torch.empty(max_out, dtype=torch.float32).pin_memory() if include_early else None,
+                "direct": torch.empty(max_ch, dtype=torch.int32).pin_memory(),
+                "done": None, "part": -1,
+            })
+        self.compute = torch.cuda.Stream(self.dev)
+        self.copy = torch.cuda.Stream(self.dev)
+
+    @property
+    def n_jobs(self) -> int:
+        return sum(len(p.jobs) for p in self.parts)
+
+    @property
+    def h2d_bytes(self) -> int:
+        return sum(p.jobs.nbytes + p.chan_job.nbytes + p.chan_order.nbytes + p.mics.nbytes for p in self.parts)
+
+    @property
+    def d2h_bytes(self) -> int:
+        v = 2 if self.include_early else 1
+        return sum(int(p.batch.total_out) * 4 * v + int(p.batch.total_channels) * 4 for p in self.parts)
+
+    def _retire(self, slot, consumer):
+        if slot["done"] is not None:
+            slot["done"].synchronize()
+            if consumer is not None:
+                k = slot["part"]
+                nout, nch = int(self.parts[k].batch.total_out), int(self.parts[k].batch.total_channels)
+                consumer(k, {"full": slot["full"].numpy()[:nout],
+                             "early": slot["early"].numpy()[:nout] if slot["early"] is not None else None,
+                             "direct": slot["direct"].numpy()[:nch]})
+            slot["done"] = None
+
+    def run(self, consumer=None, revalidate: bool = True) -> None:
+        """One end-to-end pass over every part (see the class docstring)."""
+        for k, db in enumerate(self.dbs):
+            slot = self.slots[k % len(self.slots)]
+            self._retire(slot, consumer)
+            pb = prepare(self.sample_rate, *self.src[k]) if revalidate else self.parts[k]
+            nj, nc, nm = pb.jobs.nbytes, len(pb.chan_job), pb.mics.size
+            slot["jobs"].numpy()[:nj] = pb.jobs.view(np.uint8).reshape(-1)
+            slot["chan_job"].numpy()[:nc] = pb.chan_job
+            slot["chan_order"].numpy()[:nc] = pb.chan_order
+            slot["mics"].numpy()[:nm] = pb.mics.reshape(-1)
+            nout, nch = int(pb.batch.total_out), int(pb.batch.total_channels)
+            with torch.cuda.stream(self.compute):
+                db.jobs.copy_(slot["jobs"][:nj], non_blocking=True)
+                db.chan_job.copy_(slot["chan_job"][:nc], non_blocking=True)
+                db.chan_order.copy_(slot["chan_order"][:nc], non_blocking=True)
+                db.mics.copy_(slot["mics"][:nm], non_blocking=True)
+                db.launch(slot["d_full"], slot["d_early"], slot["d_direct"], self.compute, workspace=slot["ws"])
+                ev = torch.cuda.Event()
+                ev.record(self.compute)
+            with torch.cuda.stream(self.copy):
+                self.copy.wait_event(ev)
+                slot["full"][:nout].copy_(slot["d_full"][:nout], non_blocking=True)
+                if slot["early"] is not None:
+                    slot["early"][:nout].copy_(slot["d_early"][:nout], non_blocking=True)
+                slot["direct"][:nch].copy_(slot["d_direct"][:nch], non_blocking=True)
+                done = torch.cuda.Event()
+                done.record(self.copy)
+            # (the slot's buffers are reused only after _retire() has waited for this copy)
+            slot["done"], slot["part"] = done, k
+        for slot in self.slots:
+            self._retire(slot, consumer)
