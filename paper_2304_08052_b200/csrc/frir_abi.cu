@@ -171,6 +171,12 @@ int frir_plan_create(int32_t fs, frir_plan** out) {
   for (int i = 0; i < 4; ++i) dv.mc[i] = scan[kScanStart + 4 + i];  // M^(C * 1)
   for (int i = 0; i < 2 * kChunk; ++i) dv.fr0[i] = scan[kScanFree + i];
   for (int i = 0; i < 4; ++i) dv.mt[i] = scan[kScanTileM + i];
+  if (e == cudaSuccess) e = init_launch_cache(p);
+  if (e == cudaSuccess && p->lc.render_per_sm[0][(D.d.sup + 31) / 32 - 1][0] < 1) {
+    frir_plan_destroy(p);
+    set_error("sample_rate " + std::to_string(fs) + ": the render kernel's filter tables exceed the device's shared memory");
+    return FRIR_ERANGE;
+  }
   if (e != cudaSuccess) {
     set_error(std::string("plan upload: ") + cudaGetErrorString(e));
     frir_plan_destroy(p);

@@ -53,12 +53,21 @@ struct DevPlan {
 constexpr int kScanKS = 0, kScanStart = 20, kScanFree = 20 + 128, kScanTileM = kScanFree + 2 * kTile;
 constexpr int kScanDoubles = kScanTileM + 4;
 
+// Device facts and kernel attributes queried once per plan (frir_plan_create),
+// so launches issue no attribute or occupancy queries.
+struct LaunchCache {
+  int sms = 148;
+  int smem_optin = 227 * 1024;  // max dynamic smem per block (opt-in)
+  int render_per_sm[2][2][2] = {};  // [EARLY][NBK - 1][SEG]: resident render CTAs per SM
+};
+
 }  // namespace frir
 
 struct frir_plan {
   frir::Design design;
   frir::DevPlan dev;
   int device;
+  frir::LaunchCache lc;
 };
 
 namespace frir {
@@ -68,5 +77,6 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* ws, size_t
                     int stages);
 size_t workspace_bytes(const frir_batch* b);
 int launches(const frir_batch* b, int early);
+cudaError_t init_launch_cache(frir_plan* plan);
 int check_line();
 }  // namespace frir

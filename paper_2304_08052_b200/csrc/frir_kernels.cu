@@ -77,11 +77,14 @@ inline int batch_seg_max(const frir_batch* b) {  // upper bound over the batch's
 __host__ __device__ inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
+// The raw region holds K1's unsorted item list.
+inline size_t raw_bytes(const frir_batch* b) { return align_up((size_t)b->total_items * 8); }
+
 Workspace carve(void* base, const frir_batch* b) {
   char* p = (char*)base;
   Workspace w;
   w.items = (int2*)p; p += align_up((size_t)b->total_items * 8);
-  w.items_raw = (int2*)p; p += align_up((size_t)b->total_items * 8);
+  w.items_raw = (int2*)p; p += raw_bytes(b);
   w.chan_q0 = (int*)p; p += align_up((size_t)b->total_channels * 4);
   w.chan_rows = (int*)p; p += align_up((size_t)b->total_channels * 4);
   w.chan_scale = (float*)p; p += align_up((size_t)b->total_channels * 4);
@@ -94,8 +97,8 @@ Workspace carve(void* base, const frir_batch* b) {
 SegWs carve_seg(void* base, const frir_batch* b) {
   SegWs g{nullptr, nullptr, nullptr, nullptr};
   if (batch_seg_max(b) <= 1) return g;
-  char* p = (char*)base + 2 * align_up((size_t)b->total_items * 8) + 3 * align_up((size_t)b->total_channels * 4) +
-            align_up((size_t)b->total_channels * 64 * 8) + 256;
+  char* p = (char*)base + align_up((size_t)b->total_items * 8) + raw_bytes(b) +
+            3 * align_up((size_t)b->total_channels * 4) + align_up((size_t)b->total_channels * 64 * 8) + 256;
   g.seg = (int*)p; p += align_up((size_t)b->total_channels * kSegInts * 4);
   g.state = (double*)p; p += align_up((size_t)b->total_channels * kMaxSeg * 4 * 8);
   g.units = (int*)p; p += align_up((size_t)b->total_channels * kMaxSeg * 4);
@@ -195,45 +198,13 @@ __device__ __forceinline__ int2 make_item(int q, float a, int r_h, int t0, unsig
   return make_int2((int)(spb | (phi << 20)), __float_as_int(a));
 }
 
-#ifndef FRIR_GEOM_MINB
-#define FRIR_GEOM_MINB 8
-#endif
-// Buckets of a channel's items (32-sample output windows, biased) and the
-// extra bucket after them that holds ISM arrivals past the train end
-// (ism.py:131-133 drops them): the sort puts them last and K2b / K3 stop
-// before them.
-__host__ __device__ inline int legit_buckets(int n2) { return ((n2 + kExt + kSpBias) >> 5) + 2; }
-__device__ __forceinline__ int2 dropped_item(int n2) { return make_int2(legit_buckets(n2) << 5, 0); }
-
-__global__ void __launch_bounds__(128, FRIR_GEOM_MINB) geom_kernel(GeomArgs A) {
-  const int j = blockIdx.x;
-  const frir_job& J = A.jobs[j];
-  const int I = J.n_images, rows = I + 1, M = J.n_mics;
-  const int g = blockIdx.y * blockDim.x + threadIdx.x;  // group of 4 images
-  const int ngroups = (I + 3) / 4;
-  const double* mics = A.mics + 3 * (size_t)J.mic_off;
-  const double rate_c0 = __ddiv_rn(A.rate, J.c0);
-  int2* items = A.ws.items_raw + J.item_off;
-  const int ism = J.kind == FRIR_KIND_ISM;  // 1: arrivals past L - 1 are dropped, not clamped
-  if (g == 0) {  // row 0: direct path (core.py:169, params.py:156-159), r**0 = 1
-    double x, y, z;
-    image_position(J, J.d0, J.az, J.el, &x, &y, &z);
-    for (int m = 0; m < M; ++m) {
-      double D;
-      int q = delay_of(x, y, z, mics + 3 * m, J.c0, A.rate, rate_c0, J.L + ism, &D);
-      // ISM drops arrivals past the train end (ism.py:131-133): they go to the
-      // dropped-arrival bucket; the direct index still clamps (:134-136)
-      const bool drop = q > J.L - 1;
-      q = min(q, J.L - 1);
-      items[(size_t)m * rows] = drop ? dropped_item(J.n2) : make_item(q, (float)__drcp_rn(D), A.r_h, A.t0, A.rh_magic);
-      A.ws.chan_q0[J.chan_off + m] = q;
-      A.ws.chan_scale[J.chan_off + m] = J.normalize ? (float)D : 1.0f;  // direct path -> 1/(1 m)
-      // resample.py:115-119: clip(round(q0 / r_h), 0, n2 - 1), half-even
-      int di = (int)rint(__ddiv_rn((double)q, (double)A.r_h));
-      A.direct_index[J.chan_off + m] = di < 0 ? 0 : (di > J.n2 - 1 ? J.n2 - 1 : di);
-    }
-  }
-  if (g >= ngroups) return;
+// Per-image part of K1 for images 4g + 1 .. 4g + 4 of job J: absolute image
+// positions (FP64, numpy's operation order) and the FP32 gains r^g.  Shared by
+// geom_kernel and image_kernel.
+__device__ __forceinline__ void image_group(const GeomArgs& A, const frir_job& J, int g, double (&px)[4],
+                                            double (&py)[4], double (&pz)[4], float (&lg)[4]) {
+  const int I = J.n_images;
+  const int ism = J.kind == FRIR_KIND_ISM;
   const double c_max = __dmul_rn(J.c0, J.t60);
   double th[4], ph[4], dist[4], refl[4];
   if (ism && J.lattice > 0) {
@@ -303,8 +274,6 @@ __global__ void __launch_bounds__(128, FRIR_GEOM_MINB) geom_kernel(GeomArgs A) {
       refl[k] = gg;
     }
   }
-  double px[4], py[4], pz[4];
-  float lg[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     if (J.kind == FRIR_KIND_ISM) {  // lattice images arrive as absolute positions
@@ -316,6 +285,50 @@ __global__ void __launch_bounds__(128, FRIR_GEOM_MINB) geom_kernel(GeomArgs A) {
     const double x = refl[k] * J.log2r, xi = floor(x);
     lg[k] = ldexpf(exp2f((float)(x - xi)), (int)xi);
   }
+}
+
+#ifndef FRIR_GEOM_MINB
+#define FRIR_GEOM_MINB 8
+#endif
+// Buckets of a channel's items (32-sample output windows, biased) and the
+// extra bucket after them that holds ISM arrivals past the train end
+// (ism.py:131-133 drops them): the sort puts them last and K2b / K3 stop
+// before them.
+__host__ __device__ inline int legit_buckets(int n2) { return ((n2 + kExt + kSpBias) >> 5) + 2; }
+__device__ __forceinline__ int2 dropped_item(int n2) { return make_int2(legit_buckets(n2) << 5, 0); }
+
+__global__ void __launch_bounds__(128, FRIR_GEOM_MINB) geom_kernel(GeomArgs A) {
+  const int j = blockIdx.x;
+  const frir_job& J = A.jobs[j];
+  const int I = J.n_images, rows = I + 1, M = J.n_mics;
+  const int g = blockIdx.y * blockDim.x + threadIdx.x;  // group of 4 images
+  const int ngroups = (I + 3) / 4;
+  const double* mics = A.mics + 3 * (size_t)J.mic_off;
+  const double rate_c0 = __ddiv_rn(A.rate, J.c0);
+  int2* items = A.ws.items_raw + J.item_off;
+  const int ism = J.kind == FRIR_KIND_ISM;  // 1: arrivals past L - 1 are dropped, not clamped
+  if (g == 0) {  // row 0: direct path (core.py:169, params.py:156-159), r**0 = 1
+    double x, y, z;
+    image_position(J, J.d0, J.az, J.el, &x, &y, &z);
+    for (int m = 0; m < M; ++m) {
+      double D;
+      int q = delay_of(x, y, z, mics + 3 * m, J.c0, A.rate, rate_c0, J.L + ism, &D);
+      // ISM drops arrivals past the train end (ism.py:131-133): they go to the
+      // dropped-arrival bucket; the direct index still clamps (:134-136)
+      const bool drop = q > J.L - 1;
+      q = min(q, J.L - 1);
+      items[(size_t)m * rows] = drop ? dropped_item(J.n2) : make_item(q, (float)__drcp_rn(D), A.r_h, A.t0, A.rh_magic);
+      A.ws.chan_q0[J.chan_off + m] = q;
+      A.ws.chan_scale[J.chan_off + m] = J.normalize ? (float)D : 1.0f;  // direct path -> 1/(1 m)
+      // resample.py:115-119: clip(round(q0 / r_h), 0, n2 - 1), half-even
+      int di = (int)rint(__ddiv_rn((double)q, (double)A.r_h));
+      A.direct_index[J.chan_off + m] = di < 0 ? 0 : (di > J.n2 - 1 ? J.n2 - 1 : di);
+    }
+  }
+  if (g >= ngroups) return;
+  double px[4], py[4], pz[4];
+  float lg[4];
+  image_group(A, J, g, px, py, pz, lg);
   const int r0 = 4 * g + 1;
   const int nk = min(4, I - 4 * g);
   for (int m = 0; m < M; ++m) {
@@ -353,6 +366,18 @@ __device__ __forceinline__ Cplx cmul(Cplx a, Cplx b) {
 // stage-2 window reaches past the stage-1 length n1, resample.py:107-113).
 __host__ __device__ inline int first_corrected(const frir_plan_desc& d, int n1) {
   return n1 - d.half2 > 0 ? (n1 - d.half2 + d.r_l - 1) / d.r_l : 0;
+}
+
+// Lanes of the warp holding the same key b (b < 2^kbits; distinct keys for
+// idle lanes): one ballot per key bit (MATCH.ANY measured slower on B200).
+__device__ __forceinline__ unsigned peers_of(int b, int kbits) {
+  unsigned peers = 0xffffffffu;
+  for (int k = 0; k < kbits; ++k) {
+    const bool bit = (b >> k) & 1;
+    const unsigned ones = __ballot_sync(0xffffffffu, bit);
+    peers &= bit ? ones : ~ones;
+  }
+  return peers;
 }
 
 struct SortArgs {
@@ -487,12 +512,7 @@ __global__ void __launch_bounds__(NW * 32) sort_kernel(SortArgs A) {
     const int rel = A.r_h * sp - A.t0 - phi - q0;  // q - q0
     if (rel >= -J.e_lo && rel <= J.e_hi) it.y ^= 0x80000000;  // early: negative gain
     const int b = ok ? (it.x & 0xFFFFF) >> 5 : nbk + lane;  // distinct for idle lanes
-    unsigned peers = 0xffffffffu;  // lanes with the same bucket: one ballot per key bit
-    for (int k = 0; k < kbits; ++k) {
-      const bool bit = (b >> k) & 1;
-      const unsigned ones = __ballot_sync(0xffffffffu, bit);
-      peers &= bit ? ones : ~ones;
-    }
+    const unsigned peers = peers_of(b, kbits);  // lanes with the same bucket
     const int rank = __popc(peers & ((1u << lane) - 1u));
     CT* slot = s_cnt + (ok ? b * kSortWarps + warp : 0);
     const int pos = ok ? *slot + rank : 0;
@@ -587,6 +607,43 @@ __global__ void __launch_bounds__(kTailThreads) tail_kernel(const __grid_constan
     p_hi = min(rows, p_t + chunk);
   }
   double4 z = make_double4(0.0, 0.0, 0.0, 0.0);  // this lane's partial modal sums (F, E)
+  // One straddler (taps on both sides of n1) or head item at high-rate delay qs
+  // with full / early amplitudes aF / aE, processed by the whole warp.
+  auto straddle = [&](int qs, double aF, double aE) {
+    const int khs = (int)__umulhi((unsigned)(up * qs + half1), down_magic);
+    const int xs = up * qs - half1 + 1024 * down;  // >= 0 (half1 = 10 r_h <= 1024 down)
+    const int klo = max(0, (int)__umulhi((unsigned)xs, down_magic) - 1024 + (xs % down != 0));
+    const int kend = min(khs + 1, n1);
+    for (int k = klo + lane; k < kend; k += 32) {  // taps 0 <= k < n1 feed the state
+      const int mm = n1 - 1 - k;
+      if (mm >= d.horizon) continue;
+      FRIR_CHECK(down * k + half1 - up * qs >= 0 && down * k + half1 - up * qs < d.len1);
+      const double h = P.h1up[down * k + half1 - up * qs];
+      const double2 lo = s_plo[mm & 127], hi = s_phi[mm >> 7];
+      const Cplx pm = cmul({hi.x, hi.y}, {lo.x, lo.y});
+      const double cF = aF * h, cE = aE * h;
+      z.x = fma(cF, pm.re, z.x);
+      z.y = fma(cF, pm.im, z.y);
+      z.z = fma(cE, pm.re, z.z);
+      z.w = fma(cE, pm.im, z.w);
+    }
+    for (int l = lane; l < d.lt_max; l += 32) {  // taps k >= n1: input past the truncation point
+      const int k = n1 + l;
+      if (k <= khs) {
+        const int idx = down * k + half1 - up * qs;
+        if (idx >= 0 && idx < d.len1) {
+          const double h = P.h1up[idx];
+          xt_s[l] += aF * h;
+          xt_s[ltc + l] += aE * h;
+        }
+      }
+    }
+  };
+  // Arrivals clamped to the last train sample (core.py:242-243, q = L - 1) are
+  // straddlers with identical taps: their amplitudes are summed (fixed order:
+  // per batch a shuffle tree, batches in row order) and they are processed once.
+  const int q_last = J.L - 1;
+  double clampF = 0.0, clampE = 0.0;
   constexpr int kGroup = 8;  // batches loaded together (memory-level parallelism)
   for (int p0 = p_t; p0 < p_hi; p0 += 32 * kGroup) {
   int2 grp[kGroup];
@@ -624,47 +681,31 @@ __global__ void __launch_bounds__(kTailThreads) tail_kernel(const __grid_constan
         z.w = fma(a, t.im, z.w);
       }
     }
-    // straddlers (taps on both sides of n1) and head items: one at a time
-    unsigned strad = __ballot_sync(0xffffffffu, valid && (khi >= n1 || head_item));
+    const bool strad_lane = valid && (khi >= n1 || head_item);
+    const bool clamped = strad_lane && qm == q_last && !head_item;
+    if (__any_sync(0xffffffffu, clamped)) {
+      double sF = clamped ? a : 0.0, sE = clamped && early ? a : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sF += __shfl_xor_sync(0xffffffffu, sF, o);
+        sE += __shfl_xor_sync(0xffffffffu, sE, o);
+      }
+      clampF += sF;
+      clampE += sE;
+    }
+    // other straddlers and head items: one at a time
+    unsigned strad = __ballot_sync(0xffffffffu, strad_lane && !clamped);
     while (strad) {
       const int src = __ffs(strad) - 1;
       strad &= strad - 1;
       const int qs = __shfl_sync(0xffffffffu, qm, src);
       const float aes = __int_as_float(__shfl_sync(0xffffffffu, it.y, src));
       const double as = fabs((double)aes);
-      const bool es = aes < 0.f;
-      const int khs = (int)__umulhi((unsigned)(up * qs + half1), down_magic);
-      const int xs = up * qs - half1 + 1024 * down;  // >= 0 (half1 = 10 r_h <= 1024 down)
-      const int klo = max(0, (int)__umulhi((unsigned)xs, down_magic) - 1024 + (xs % down != 0));
-      const int kend = min(khs + 1, n1);
-      for (int k = klo + lane; k < kend; k += 32) {  // taps 0 <= k < n1 feed the state
-        const int mm = n1 - 1 - k;
-        if (mm >= d.horizon) continue;
-        FRIR_CHECK(down * k + half1 - up * qs >= 0 && down * k + half1 - up * qs < d.len1);
-        const double cc = as * P.h1up[down * k + half1 - up * qs];
-        const double2 lo = s_plo[mm & 127], hi = s_phi[mm >> 7];
-        const Cplx pm = cmul({hi.x, hi.y}, {lo.x, lo.y});
-        z.x = fma(cc, pm.re, z.x);
-        z.y = fma(cc, pm.im, z.y);
-        if (es) {
-          z.z = fma(cc, pm.re, z.z);
-          z.w = fma(cc, pm.im, z.w);
-        }
-      }
-      for (int l = lane; l < d.lt_max; l += 32) {  // taps k >= n1: input past the truncation point
-        const int k = n1 + l;
-        if (k <= khs) {
-          const int idx = down * k + half1 - up * qs;
-          if (idx >= 0 && idx < d.len1) {
-            const double cc = as * P.h1up[idx];
-            xt_s[l] += cc;
-            if (es) xt_s[ltc + l] += cc;
-          }
-        }
-      }
+      straddle(qs, as, aes < 0.f ? as : 0.0);
     }
   }
   }  // groups
+  if (clampF != 0.0 || clampE != 0.0) straddle(q_last, clampF, clampE);  // (warp-uniform)
   // boundary state s = 2 Re(v0 zeta) and the corrections of outputs n_c + lane
   Cplx zF = {z.x, z.y}, zE = {z.z, z.w};
 #pragma unroll
@@ -1218,7 +1259,7 @@ int check_line() {
 }
 
 size_t workspace_bytes(const frir_batch* b) {
-  size_t n = 2 * align_up((size_t)b->total_items * 8) + 3 * align_up((size_t)b->total_channels * 4) +
+  size_t n = align_up((size_t)b->total_items * 8) + raw_bytes(b) + 3 * align_up((size_t)b->total_channels * 4) +
              align_up((size_t)b->total_channels * 64 * 8) + 256;
   const int smax = batch_seg_max(b);
   if (smax > 1)
@@ -1228,6 +1269,7 @@ size_t workspace_bytes(const frir_batch* b) {
 }
 
 static int table_blocks(const frir_plan_desc& d) { return (d.sup + 31) / 32; }
+constexpr int kDynSlack = 1024;  // >= any kernel's static smem; launches check sizes against optin - slack
 
 static size_t render_smem(const frir_plan_desc& d, bool early) {
   const int v = early ? 2 : 1;
@@ -1236,20 +1278,65 @@ static size_t render_smem(const frir_plan_desc& d, bool early) {
          (size_t)kWarps * v * 2 * 64 * 4;
 }
 
-template <bool EARLY, int NBK, bool SEG>
-static cudaError_t launch_render(const RenderArgs& ra, const frir_plan_desc& d, long channels,
-                                 cudaStream_t st) {
-  size_t smem = render_smem(d, EARLY);
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaError_t e = cudaFuncSetAttribute(render_kernel<EARLY, NBK, SEG>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+// Dynamic smem cap of every kernel: the opt-in maximum minus its static smem.
+template <typename K>
+static cudaError_t allow_smem(K k, int optin) {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, k);
   if (e != cudaSuccess) return e;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, render_kernel<EARLY, NBK, SEG>, kRenderThreads, smem);
-  if (per_sm < 1) per_sm = 1;
+  return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+}
+
+// Every kernel that takes dynamic shared memory gets the device's opt-in
+// maximum once here, and the render kernels' residency is queried once, so a
+// launch issues no attribute or occupancy calls (plan = one device).
+template <bool EARLY, int NBK, bool SEG>
+static cudaError_t init_render(frir_plan* p) {
+  auto k = render_kernel<EARLY, NBK, SEG>;
+  const size_t smem = render_smem(p->dev.d, EARLY);
+  int& per_sm = p->lc.render_per_sm[EARLY][NBK - 1][SEG];
+  per_sm = 0;
+  if ((int)smem > p->lc.smem_optin - kDynSlack) return cudaSuccess;  // 0: this plan cannot launch it
+  // the cap is per kernel, not per plan: plans of other rates launch it with other sizes
+  cudaError_t e = allow_smem(k, p->lc.smem_optin);
+  if (e != cudaSuccess) return e;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kRenderThreads, smem);
+  return e;
+}
+
+cudaError_t init_launch_cache(frir_plan* p) {
+  LaunchCache& lc = p->lc;
+  cudaError_t e = cudaDeviceGetAttribute(&lc.sms, cudaDevAttrMultiProcessorCount, p->device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&lc.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device);
+  const int mx = lc.smem_optin;
+  if (e == cudaSuccess) e = allow_smem(sort_kernel<uint16_t, 8, false>, mx);
+  if (e == cudaSuccess) e = allow_smem(sort_kernel<uint16_t, 16, false>, mx);
+  if (e == cudaSuccess) e = allow_smem(sort_kernel<uint32_t, 8, false>, mx);
+  if (e == cudaSuccess) e = allow_smem(sort_kernel<uint32_t, 16, false>, mx);
+  if (e == cudaSuccess) e = allow_smem(sort_kernel<uint16_t, 8, true>, mx);
+  if (e == cudaSuccess) e = allow_smem(sort_kernel<uint16_t, 16, true>, mx);
+  if (e == cudaSuccess) e = allow_smem(sort_kernel<uint32_t, 8, true>, mx);
+  if (e == cudaSuccess) e = allow_smem(sort_kernel<uint32_t, 16, true>, mx);
+  if (e == cudaSuccess) e = allow_smem(tail_kernel<false>, mx);
+  if (e == cudaSuccess) e = allow_smem(tail_kernel<true>, mx);
+  if (e == cudaSuccess) e = init_render<true, 1, false>(p);
+  if (e == cudaSuccess) e = init_render<true, 1, true>(p);
+  if (e == cudaSuccess) e = init_render<false, 1, false>(p);
+  if (e == cudaSuccess) e = init_render<false, 1, true>(p);
+  if (e == cudaSuccess) e = init_render<true, 2, false>(p);
+  if (e == cudaSuccess) e = init_render<true, 2, true>(p);
+  if (e == cudaSuccess) e = init_render<false, 2, false>(p);
+  if (e == cudaSuccess) e = init_render<false, 2, true>(p);
+  return e;
+}
+
+template <bool EARLY, int NBK, bool SEG>
+static cudaError_t launch_render(const frir_plan* plan, const RenderArgs& ra, long channels, cudaStream_t st) {
+  const size_t smem = render_smem(plan->dev.d, EARLY);
+  const int per_sm = plan->lc.render_per_sm[EARLY][NBK - 1][SEG];
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
   long want = (channels * ra.seg_max + kWarps - 1) / kWarps;  // upper bound of the work units
-  int grid = (int)std::min<long>((long)sms * per_sm, want);
+  int grid = (int)std::min<long>((long)plan->lc.sms * per_sm, want);
   render_kernel<EARLY, NBK, SEG><<<grid, kRenderThreads, smem, st>>>(ra);
   return cudaGetLastError();
 }
@@ -1280,14 +1367,14 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_
   cudaError_t e = cudaSuccess;
 
   const int rate = d.r_h * d.sample_rate;
+  GeomArgs ga;
+  ga.jobs = b->jobs; ga.mics = b->mics;
+  ga.draw_dist = b->draw_dist; ga.draw_az = b->draw_az; ga.draw_el = b->draw_el; ga.draw_refl = b->draw_refl;
+  ga.ws = ws; ga.direct_index = direct_index;
+  ga.r_h = d.r_h; ga.t0 = d.t0;
+  ga.rh_magic = (unsigned)((0x100000000ull + d.r_h - 1) / d.r_h);
+  ga.rate = (double)rate;
   if (stages & FRIR_STAGE_GEOM) {  // K1: draws, geometry, delays, items
-    GeomArgs ga;
-    ga.jobs = b->jobs; ga.mics = b->mics;
-    ga.draw_dist = b->draw_dist; ga.draw_az = b->draw_az; ga.draw_el = b->draw_el; ga.draw_refl = b->draw_refl;
-    ga.ws = ws; ga.direct_index = direct_index;
-    ga.r_h = d.r_h; ga.t0 = d.t0;
-    ga.rh_magic = (unsigned)((0x100000000ull + d.r_h - 1) / d.r_h);
-    ga.rate = (double)rate;
     int maxg = (b->max_rows - 1 + 3) / 4;
     dim3 g1(b->n_jobs, maxg > 0 ? (maxg + 127) / 128 : 1);
     geom_kernel<<<g1, 128, 0, st>>>(ga);
@@ -1296,72 +1383,74 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_
   }
 
   if (stages & FRIR_STAGE_DELAY) {  // K2: early flags + stable bucket sort per channel
-    SortArgs sa;
-    sa.jobs = b->jobs; sa.chan_job = b->chan_job; sa.ws = ws; sa.sw = sw;
-    sa.r_h = d.r_h; sa.t0 = d.t0; sa.plan = plan->dev;
-    const int nbk = ((b->max_windows * kWin + kSpBias) >> 5) + 3;
-    if (sw.nextra) {
-      e = cudaMemsetAsync(sw.nextra, 0, sizeof(int), st);
-      if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FRIR_ECUDA; }
-    }
-    const bool wide = b->max_rows > 65535;  // sorted positions need 32-bit counters
-    const bool big = b->total_items >= 4096LL * b->total_channels;  // long rows on average: 16 warps
-    const int nw = big ? 16 : 8;
-    const size_t smem = align16((size_t)nbk * nw * (wide ? 4 : 2));
-    auto kern = sw.seg ? (wide ? (big ? sort_kernel<uint32_t, 16, true> : sort_kernel<uint32_t, 8, true>)
-                               : (big ? sort_kernel<uint16_t, 16, true> : sort_kernel<uint16_t, 8, true>))
-                       : (wide ? (big ? sort_kernel<uint32_t, 16, false> : sort_kernel<uint32_t, 8, false>)
-                               : (big ? sort_kernel<uint16_t, 16, false> : sort_kernel<uint16_t, 8, false>));
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) {
+    {
+      SortArgs sa;
+      sa.jobs = b->jobs; sa.chan_job = b->chan_job; sa.ws = ws; sa.sw = sw;
+      sa.r_h = d.r_h; sa.t0 = d.t0; sa.plan = plan->dev;
+      const int nbk = ((b->max_windows * kWin + kSpBias) >> 5) + 3;
+      if (sw.nextra) {
+        e = cudaMemsetAsync(sw.nextra, 0, sizeof(int), st);
+        if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FRIR_ECUDA; }
+      }
+      const bool wide = b->max_rows > 65535;  // sorted positions need 32-bit counters
+      const bool big = b->total_items >= 4096LL * b->total_channels;  // long rows on average: 16 warps
+      int nw = big ? 16 : 8;
+      size_t smem = align16((size_t)nbk * nw * (wide ? 4 : 2));
+      const size_t cap = (size_t)(plan->lc.smem_optin - kDynSlack);
+      if (smem > cap && nw == 16) {  // fewer warps, fewer counters
+        nw = 8;
+        smem = align16((size_t)nbk * nw * (wide ? 4 : 2));
+      }
+      if (smem > cap) {
+        set_error("RIR too long for the per-channel sort: " + std::to_string(nbk) + " buckets need " +
+                  std::to_string(smem) + " bytes of shared memory");
+        return FRIR_ERANGE;
+      }
+      auto kern = sw.seg ? (wide ? (nw == 16 ? sort_kernel<uint32_t, 16, true> : sort_kernel<uint32_t, 8, true>)
+                                 : (nw == 16 ? sort_kernel<uint16_t, 16, true> : sort_kernel<uint16_t, 8, true>))
+                         : (wide ? (nw == 16 ? sort_kernel<uint32_t, 16, false> : sort_kernel<uint32_t, 8, false>)
+                                 : (nw == 16 ? sort_kernel<uint16_t, 16, false> : sort_kernel<uint16_t, 8, false>));
       kern<<<b->total_channels, nw * 32, smem, st>>>(sa);
       e = cudaGetLastError();
+      if (e != cudaSuccess) { set_error(std::string("sort_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
     }
-    if (e != cudaSuccess) { set_error(std::string("sort_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
     TailArgs ta;  // K2b: tail corrections from the sorted rows
     ta.jobs = b->jobs; ta.chan_job = b->chan_job; ta.ws = ws; ta.sw = sw; ta.plan = plan->dev;
     ta.total_channels = b->total_channels;
     const size_t tsm = tail_smem(d);
-    e = cudaFuncSetAttribute(tail_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
-    if (e == cudaSuccess && sw.seg) e = cudaFuncSetAttribute(tail_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
-    if (e == cudaSuccess) {
-      tail_kernel<false><<<(b->total_channels + kTailWarps - 1) / kTailWarps, kTailThreads, tsm, st>>>(ta);
-      if (sw.seg) tail_kernel<true><<<b->total_channels, kTailThreads, tsm, st>>>(ta);  // long channels
-      e = cudaGetLastError();
-    }
+    tail_kernel<false><<<(b->total_channels + kTailWarps - 1) / kTailWarps, kTailThreads, tsm, st>>>(ta);
+    if (sw.seg) tail_kernel<true><<<b->total_channels, kTailThreads, tsm, st>>>(ta);  // long channels
+    e = cudaGetLastError();
     if (e != cudaSuccess) { set_error(std::string("tail_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
   }
 
   if (stages & FRIR_STAGE_RENDER) {  // K3
-  e = cudaMemsetAsync(ws.counter, 0, sizeof(int), st);
-  if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FRIR_ECUDA; }
-  RenderArgs ra;
-  ra.jobs = b->jobs; ra.chan_job = b->chan_job; ra.chan_order = b->chan_order;
-  ra.total_channels = b->total_channels; ra.ws = ws; ra.sw = sw; ra.plan = plan->dev;
-  ra.out_full = out_full; ra.out_early = out_early;
-  ra.seg_max = batch_seg_max(b);
-  const bool early = out_early != nullptr;
-  const int nbk = table_blocks(d);
-  const bool seg = ra.seg_max > 1;
-  if (nbk == 1)
-    e = early ? (seg ? launch_render<true, 1, true>(ra, d, b->total_channels, st)
-                     : launch_render<true, 1, false>(ra, d, b->total_channels, st))
-              : (seg ? launch_render<false, 1, true>(ra, d, b->total_channels, st)
-                     : launch_render<false, 1, false>(ra, d, b->total_channels, st));
-  else
-    e = early ? (seg ? launch_render<true, 2, true>(ra, d, b->total_channels, st)
-                     : launch_render<true, 2, false>(ra, d, b->total_channels, st))
-              : (seg ? launch_render<false, 2, true>(ra, d, b->total_channels, st)
-                     : launch_render<false, 2, false>(ra, d, b->total_channels, st));
-  if (e != cudaSuccess) { set_error(std::string("render_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
-  if (ra.seg_max > 1) {  // K4: seams of segmented channels
-    SeamArgs sa;
-    sa.jobs = b->jobs; sa.chan_job = b->chan_job; sa.ws = ws; sa.sw = sw; sa.plan = plan->dev;
-    sa.out_full = out_full; sa.out_early = out_early; sa.total_channels = b->total_channels;
-    seam_kernel<<<(b->total_channels + 7) / 8, 256, 0, st>>>(sa);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) { set_error(std::string("seam_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
-  }
+    e = cudaMemsetAsync(ws.counter, 0, sizeof(int), st);
+    if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FRIR_ECUDA; }
+    RenderArgs ra;
+    ra.jobs = b->jobs; ra.chan_job = b->chan_job; ra.chan_order = b->chan_order;
+    ra.total_channels = b->total_channels; ra.ws = ws; ra.sw = sw; ra.plan = plan->dev;
+    ra.out_full = out_full; ra.out_early = out_early;
+    ra.seg_max = batch_seg_max(b);
+    const bool early = out_early != nullptr;
+    const int nbk = table_blocks(d);
+    const bool seg = ra.seg_max > 1;
+    const long ch = b->total_channels;
+    if (nbk == 1)
+      e = early ? (seg ? launch_render<true, 1, true>(plan, ra, ch, st) : launch_render<true, 1, false>(plan, ra, ch, st))
+                : (seg ? launch_render<false, 1, true>(plan, ra, ch, st) : launch_render<false, 1, false>(plan, ra, ch, st));
+    else
+      e = early ? (seg ? launch_render<true, 2, true>(plan, ra, ch, st) : launch_render<true, 2, false>(plan, ra, ch, st))
+                : (seg ? launch_render<false, 2, true>(plan, ra, ch, st) : launch_render<false, 2, false>(plan, ra, ch, st));
+    if (e != cudaSuccess) { set_error(std::string("render_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
+    if (ra.seg_max > 1) {  // K4: seams of segmented channels
+      SeamArgs sa;
+      sa.jobs = b->jobs; sa.chan_job = b->chan_job; sa.ws = ws; sa.sw = sw; sa.plan = plan->dev;
+      sa.out_full = out_full; sa.out_early = out_early; sa.total_channels = b->total_channels;
+      seam_kernel<<<(b->total_channels + 7) / 8, 256, 0, st>>>(sa);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) { set_error(std::string("seam_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
+    }
   }
   return FRIR_OK;
 }
