@@ -289,6 +289,14 @@ int frir_edc(const float* h, int64_t ld, const int32_t* len, int32_t C, double* 
 int frir_t60(const float* h, int64_t ld, const int32_t* len, int32_t C, const double* edc, int64_t ld_e,
              const double* amax, double sample_rate, double max_drop, double floor_margin, double min_drop,
              double* t60, void* stream);
+/* The same two entry points on float64 rows (the reference works in FP64,
+   decay.py:11-17): squares and sums in FP64 from the FP64 samples, so the
+   curve is bit-identical to numpy's for any input the reference accepts. */
+int frir_edc_f64(const double* h, int64_t ld, const int32_t* len, int32_t C, double* edc, int64_t ld_out,
+                 double* amax, void* stream);
+int frir_t60_f64(const double* h, int64_t ld, const int32_t* len, int32_t C, const double* edc, int64_t ld_e,
+                 const double* amax, double sample_rate, double max_drop, double floor_margin, double min_drop,
+                 double* t60, void* stream);
 
 const char* frir_last_error(void);
 int32_t frir_abi_version(void);

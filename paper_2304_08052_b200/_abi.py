@@ -120,6 +120,10 @@ SIGNATURES = [
     ("frir_t60", c_int32,
      [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_int64, c_void_p, c_double, c_double, c_double,
       c_double, c_void_p, c_void_p]),
+    ("frir_edc_f64", c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_int64, c_void_p, c_void_p]),
+    ("frir_t60_f64", c_int32,
+     [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_int64, c_void_p, c_double, c_double, c_double,
+      c_double, c_void_p, c_void_p]),
     ("frir_last_error", ctypes.c_char_p, []),
     ("frir_abi_version", c_int32, []),
     ("frir_struct_size", c_int64, [c_int32]),

@@ -23,11 +23,17 @@ namespace {
 constexpr int kEdcRows = 32;    // channels per CTA; lane = channel in the sums
 constexpr int kEdcTile = 64;    // samples per staged tile
 constexpr int kEdcStages = 8;   // input tiles in flight (cp.async ring)
-constexpr int kEdcIn = kEdcTile + 4;   // padded input row: 16-byte aligned, 4-way banks
 constexpr int kEdcOut = kEdcTile + 2;  // padded output row: 16-byte aligned
 constexpr int kEdcIo = 4;               // I/O warps per CTA (plus one summing warp)
-constexpr size_t kEdcSmem = (size_t)kEdcStages * kEdcRows * kEdcIn * 4 + 2 * (size_t)kEdcRows * kEdcOut * 8 +
-                            kEdcRows * 4;
+// Input samples are float32 (renderer output) or float64 (any caller's rows,
+// e.g. the reference's own RIRs): VEC elements per 16-byte copy, padded rows.
+template <typename T>
+struct EdcIn {
+  static constexpr int kVec = 16 / (int)sizeof(T);
+  static constexpr int kRow = kEdcTile + kVec;  // padded input row: 16-byte aligned
+  static constexpr size_t kSmem = (size_t)kEdcStages * kEdcRows * kRow * sizeof(T) +
+                                  2 * (size_t)kEdcRows * kEdcOut * 8 + kEdcRows * 4;
+};
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -45,15 +51,17 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // zero-filled past each length; scalar loads when rows are not 16-byte
 // aligned) and writes the previous EDC tile out row-contiguous, so the serial
 // sums never wait on memory.
-__global__ void __launch_bounds__(32 * (1 + kEdcIo)) edc_kernel(const float* __restrict__ h, long ld,
+template <typename T>
+__global__ void __launch_bounds__(32 * (1 + kEdcIo)) edc_kernel(const T* __restrict__ h, long ld,
                                                  const int32_t* __restrict__ len, int C,
                                                  double* __restrict__ edc, long ld_out,
                                                  double* __restrict__ amax) {
+  constexpr int kEdcIn = EdcIn<T>::kRow, kVec = EdcIn<T>::kVec;
   extern __shared__ __align__(16) unsigned char edc_smem[];
-  float(*tin)[kEdcRows][kEdcIn] = reinterpret_cast<float(*)[kEdcRows][kEdcIn]>(edc_smem);
+  T(*tin)[kEdcRows][kEdcIn] = reinterpret_cast<T(*)[kEdcRows][kEdcIn]>(edc_smem);
   double(*tout)[kEdcRows][kEdcOut] =
-      reinterpret_cast<double(*)[kEdcRows][kEdcOut]>(edc_smem + (size_t)kEdcStages * kEdcRows * kEdcIn * 4);
-  int* s_len = reinterpret_cast<int*>(edc_smem + (size_t)kEdcStages * kEdcRows * kEdcIn * 4 +
+      reinterpret_cast<double(*)[kEdcRows][kEdcOut]>(edc_smem + (size_t)kEdcStages * kEdcRows * kEdcIn * sizeof(T));
+  int* s_len = reinterpret_cast<int*>(edc_smem + (size_t)kEdcStages * kEdcRows * kEdcIn * sizeof(T) +
                                       2 * (size_t)kEdcRows * kEdcOut * 8);
   const int c0 = blockIdx.x * kEdcRows;
   const int lane = threadIdx.x & 31;
@@ -65,24 +73,25 @@ __global__ void __launch_bounds__(32 * (1 + kEdcIo)) edc_kernel(const float* __r
   for (int r = 0; r < kEdcRows; ++r) nmax = max(nmax, s_len[r]);
   const int ntile = (int)((max((long)nmax, ld_out) + kEdcTile - 1) / kEdcTile);
   const int nlive = (nmax + kEdcTile - 1) / kEdcTile;  // tiles holding samples
-  const bool vec_in = (ld % 4 == 0) && (((uintptr_t)h & 15) == 0);
+  const bool vec_in = (ld % kVec == 0) && (((uintptr_t)h & 15) == 0);
   const bool vec_out = (ld_out % 2 == 0) && (((uintptr_t)edc & 15) == 0);
 
   auto stage = [&](int t) {  // I/O warp: tile t into ring slot t % kEdcStages
     if (t >= 0 && t < nlive) {
       const int base = t * kEdcTile;
-      float(*dst)[kEdcIn] = tin[t % kEdcStages];
+      T(*dst)[kEdcIn] = tin[t % kEdcStages];
+      constexpr int kPerRow = kEdcTile / kVec;  // 16-byte copies per row
 #pragma unroll
-      for (int i = 0; i < kEdcRows * kEdcTile / 4 / (32 * kEdcIo); ++i) {
-        const int q = (i * kEdcIo + iw) * 32 + lane, r = q >> 4, col = (q & 15) * 4;
+      for (int i = 0; i < kEdcRows * kPerRow / (32 * kEdcIo); ++i) {
+        const int q = (i * kEdcIo + iw) * 32 + lane, r = q / kPerRow, col = (q % kPerRow) * kVec;
         const int nr = s_len[r];
         const long off = (long)(c0 + r) * ld + base + col;
         if (vec_in) {
-          const int bytes = max(0, min(16, (nr - base - col) * 4));
+          const int bytes = max(0, min(16, (nr - base - col) * (int)sizeof(T)));
           cp_async16(&dst[r][col], bytes > 0 ? (const void*)(h + off) : (const void*)h, bytes);
         } else {
 #pragma unroll
-          for (int e = 0; e < 4; ++e) dst[r][col + e] = base + col + e < nr ? h[off + e] : 0.f;
+          for (int e = 0; e < kVec; ++e) dst[r][col + e] = base + col + e < nr ? h[off + e] : (T)0;
         }
       }
     }
@@ -109,12 +118,12 @@ __global__ void __launch_bounds__(32 * (1 + kEdcIo)) edc_kernel(const float* __r
     __syncwarp();
   }
   double acc = 0.0;
-  float mx = 0.f;  // |h| is a float: the max is exact in FP32
+  T mx = 0;  // max |h|, exact in the input type
   for (int t = ntile - 1; t >= -1; --t) {
     __syncthreads();  // tile t staged; tout[t & 1] free (its store was two rounds ago)
     if (!io) {
       if (t >= 0 && t < nlive) {
-        const float(*src)[kEdcIn] = tin[t % kEdcStages];
+        const T(*src)[kEdcIn] = tin[t % kEdcStages];
         double* dst = tout[t & 1][lane];
         // No length tests: samples past a row's end were staged as zeros and
         // come first in the backward walk, so they leave acc at +0.0 and
@@ -126,14 +135,14 @@ __global__ void __launch_bounds__(32 * (1 + kEdcIo)) edc_kernel(const float* __r
         for (int hh = 1; hh >= 0; --hh) {
           double sq[kEdcTile / 2];
 #pragma unroll
-          for (int k = 0; k < kEdcTile / 2; k += 4) {  // 16-byte reads: conflict-free per quarter warp
-            const float4 f4 = *reinterpret_cast<const float4*>(&src[lane][hh * (kEdcTile / 2) + k]);
-            const float f[4] = {f4.x, f4.y, f4.z, f4.w};
+          for (int k = 0; k < kEdcTile / 2; k += kVec) {  // 16-byte reads
+            T f[kVec];
+            *reinterpret_cast<float4*>(f) = *reinterpret_cast<const float4*>(&src[lane][hh * (kEdcTile / 2) + k]);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
+            for (int e = 0; e < kVec; ++e) {
               const double v = (double)f[e];
-              sq[k + e] = v * v;
-              mx = fmaxf(mx, fabsf(f[e]));
+              sq[k + e] = v * v;  // numpy: h ** 2 in FP64 (exact for float32 samples)
+              mx = f[e] < 0 ? (-f[e] > mx ? -f[e] : mx) : (f[e] > mx ? f[e] : mx);
             }
           }
 #pragma unroll
@@ -161,7 +170,8 @@ __device__ __forceinline__ double db_of(double e, double e0) {
 }
 
 // measure_t60 (decay.py:20-49) per channel from the EDC and |h|.
-__global__ void t60_kernel(const float* __restrict__ h, long ld, const int32_t* __restrict__ len, int C,
+template <typename T>
+__global__ void t60_kernel(const T* __restrict__ h, long ld, const int32_t* __restrict__ len, int C,
                            const double* __restrict__ edc, long ld_e, const double* __restrict__ amax,
                            double fs, double max_drop, double floor_margin, double min_drop,
                            double* __restrict__ t60) {
@@ -175,7 +185,7 @@ __global__ void t60_kernel(const float* __restrict__ h, long ld, const int32_t* 
   }
   const double e0 = e[0];
   const double half = 0.5 * amax[c];
-  const float* row = h + (size_t)c * ld;
+  const T* row = h + (size_t)c * ld;
   int direct = 0;
   while (direct < n && !(fabs((double)row[direct]) >= half)) ++direct;
   const double d0 = db_of(e[direct], e0);
@@ -198,38 +208,62 @@ __global__ void t60_kernel(const float* __restrict__ h, long ld, const int32_t* 
 
 using namespace frir;
 
-extern "C" {
-
-int frir_edc(const float* h, int64_t ld, const int32_t* len, int32_t C, double* edc, int64_t ld_out,
-             double* amax, void* stream) {
+template <typename T>
+static int edc_impl(const T* h, int64_t ld, const int32_t* len, int32_t C, double* edc, int64_t ld_out,
+                    double* amax, void* stream) {
   if (!h || !len || !edc || !amax || C < 0 || ld < 0 || ld_out < 0) {
     set_error("frir_edc: invalid argument");
     return FRIR_EINVAL;
   }
   if (C == 0) return FRIR_OK;
   // > 48 KB of dynamic shared memory (per device and function: set every call)
-  cudaFuncSetAttribute(edc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEdcSmem);
-  edc_kernel<<<(C + kEdcRows - 1) / kEdcRows, 32 * (1 + kEdcIo), kEdcSmem, (cudaStream_t)stream>>>(
+  cudaFuncSetAttribute(edc_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EdcIn<T>::kSmem);
+  edc_kernel<T><<<(C + kEdcRows - 1) / kEdcRows, 32 * (1 + kEdcIo), EdcIn<T>::kSmem, (cudaStream_t)stream>>>(
       h, (long)ld, len, C, edc, (long)ld_out, amax);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { set_error(std::string("edc_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
   return FRIR_OK;
 }
 
-int frir_t60(const float* h, int64_t ld, const int32_t* len, int32_t C, const double* edc, int64_t ld_e,
-             const double* amax, double sample_rate, double max_drop, double floor_margin, double min_drop,
-             double* t60, void* stream) {
+template <typename T>
+static int t60_impl(const T* h, int64_t ld, const int32_t* len, int32_t C, const double* edc, int64_t ld_e,
+                    const double* amax, double sample_rate, double max_drop, double floor_margin, double min_drop,
+                    double* t60, void* stream) {
   if (!h || !len || !edc || !amax || !t60 || C < 0 || !(sample_rate > 0)) {
     set_error("frir_t60: invalid argument");
     return FRIR_EINVAL;
   }
   if (C == 0) return FRIR_OK;
-  t60_kernel<<<(C + 127) / 128, 128, 0, (cudaStream_t)stream>>>(h, (long)ld, len, C, edc, (long)ld_e, amax,
-                                                                sample_rate, max_drop, floor_margin, min_drop,
-                                                                t60);
+  t60_kernel<T><<<(C + 127) / 128, 128, 0, (cudaStream_t)stream>>>(h, (long)ld, len, C, edc, (long)ld_e, amax,
+                                                                   sample_rate, max_drop, floor_margin, min_drop,
+                                                                   t60);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { set_error(std::string("t60_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
   return FRIR_OK;
+}
+
+extern "C" {
+
+int frir_edc(const float* h, int64_t ld, const int32_t* len, int32_t C, double* edc, int64_t ld_out,
+             double* amax, void* stream) {
+  return edc_impl(h, ld, len, C, edc, ld_out, amax, stream);
+}
+
+int frir_edc_f64(const double* h, int64_t ld, const int32_t* len, int32_t C, double* edc, int64_t ld_out,
+                 double* amax, void* stream) {
+  return edc_impl(h, ld, len, C, edc, ld_out, amax, stream);
+}
+
+int frir_t60(const float* h, int64_t ld, const int32_t* len, int32_t C, const double* edc, int64_t ld_e,
+             const double* amax, double sample_rate, double max_drop, double floor_margin, double min_drop,
+             double* t60, void* stream) {
+  return t60_impl(h, ld, len, C, edc, ld_e, amax, sample_rate, max_drop, floor_margin, min_drop, t60, stream);
+}
+
+int frir_t60_f64(const double* h, int64_t ld, const int32_t* len, int32_t C, const double* edc, int64_t ld_e,
+                 const double* amax, double sample_rate, double max_drop, double floor_margin, double min_drop,
+                 double* t60, void* stream) {
+  return t60_impl(h, ld, len, C, edc, ld_e, amax, sample_rate, max_drop, floor_margin, min_drop, t60, stream);
 }
 
 }  // extern "C"

@@ -266,8 +266,9 @@ __device__ __forceinline__ void image_group(const GeomArgs& A, const frir_job& J
       // core.py:215-220 reflection counts (stage-1 stream)
       double pr = __dadd_rn(J.perturb_lo, __dmul_rn(prange, u64_to_unit(bq.v[k])));
       double qq = __ddiv_rn(dd, c_max);
-      // dr**tau only shapes the gain exponent: FP32 (rel. err ~1e-7 -> gain ~1e-9)
-      const double drt = (double)exp2f((float)J.tau * log2f((float)dr));
+      // dr**tau in FP64 (core.py:219): two correctly rounded square roots for
+      // the default tau = 0.25 (<= 1 ulp from numpy's pow), pow otherwise
+      const double drt = J.tau == 0.25 ? __dsqrt_rn(__dsqrt_rn(dr)) : pow(dr, J.tau);
       double gg = __dadd_rn(__dadd_rn(1.0, __dmul_rn(__dmul_rn(qq, qq), rrm1)), __dmul_rn(pr, drt));
       gg = fmin(fmax(gg, 1.0), J.rr_max);
       dist[k] = dd;

@@ -25,14 +25,18 @@ def _torch():
 
 
 def _rows(h, lengths, device):
+    """(C, n) device rows, float32 or float64 (kept: float64 input stays FP64;
+    other dtypes become float32, the renderer's type)."""
     torch = _torch()
     if not isinstance(h, torch.Tensor):
-        h = torch.as_tensor(np.ascontiguousarray(np.atleast_2d(h), dtype=np.float32))
+        a = np.atleast_2d(np.asarray(h))
+        a = np.ascontiguousarray(a, dtype=np.float64 if a.dtype == np.float64 else np.float32)
+        h = torch.as_tensor(a)
     if h.dim() == 1:
         h = h[None, :]
     dev = torch.device(device) if device is not None else (
         h.device if h.is_cuda else torch.device("cuda", torch.cuda.current_device()))
-    h = h.to(dev, torch.float32)
+    h = h.to(dev, torch.float64 if h.dtype == torch.float64 else torch.float32)
     if h.stride(-1) != 1:
         h = h.contiguous()
     C, n = h.shape
@@ -48,14 +52,16 @@ def _edc(h, lens, dev):
     edc = torch.empty((C, n), dtype=torch.float64, device=dev)  # frir_edc zero-fills past each length
     amax = torch.empty(C, dtype=torch.float64, device=dev)
     st = torch.cuda.current_stream(dev).cuda_stream
-    _abi.check(_abi.lib().frir_edc(h.data_ptr(), h.stride(0), lens.data_ptr(), C, edc.data_ptr(), n,
-                                   amax.data_ptr(), st), "frir_edc")
+    fn = _abi.lib().frir_edc_f64 if h.dtype == torch.float64 else _abi.lib().frir_edc
+    _abi.check(fn(h.data_ptr(), h.stride(0), lens.data_ptr(), C, edc.data_ptr(), n, amax.data_ptr(), st),
+               "frir_edc")
     return edc, amax
 
 
 def schroeder_batch(h, lengths=None, device=None):
     """Normalised energy decay curves of C rows (C, n) -> (C, n) FP64 device
-    tensor (zeros past each row's length); rows without energy give NaN rows."""
+    tensor (zeros past each row's length); rows without energy give NaN rows.
+    float64 rows are processed in FP64, anything else as float32."""
     h, lens, dev = _rows(h, lengths, device)
     edc, _ = _edc(h, lens, dev)
     return edc / edc[:, :1]
@@ -71,9 +77,10 @@ def measure_t60_batch(h, sample_rate: int, lengths=None, max_drop: float = 55.0,
     C, n = h.shape
     out = torch.empty(C, dtype=torch.float64, device=dev)
     st = torch.cuda.current_stream(dev).cuda_stream
-    _abi.check(_abi.lib().frir_t60(h.data_ptr(), h.stride(0), lens.data_ptr(), C, edc.data_ptr(), n,
-                                   amax.data_ptr(), float(sample_rate), float(max_drop), float(floor_margin),
-                                   float(min_drop), out.data_ptr(), st), "frir_t60")
+    fn = _abi.lib().frir_t60_f64 if h.dtype == torch.float64 else _abi.lib().frir_t60
+    _abi.check(fn(h.data_ptr(), h.stride(0), lens.data_ptr(), C, edc.data_ptr(), n, amax.data_ptr(),
+                  float(sample_rate), float(max_drop), float(floor_margin), float(min_drop), out.data_ptr(), st),
+               "frir_t60")
     return out
 
 
@@ -88,8 +95,8 @@ def _single(h):
 
 def schroeder_curve(h) -> np.ndarray:
     """Backward-integrated squared response normalised to 1 at the first
-    sample (decay.py:8-17).  The device works on float32 samples, as the
-    renderer produces them."""
+    sample (decay.py:8-17), in FP64 from the float64 samples like the
+    reference (bit-identical)."""
     h = _single(h)
     return schroeder_batch(h[None, :])[0].cpu().numpy()
 

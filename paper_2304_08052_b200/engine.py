@@ -165,16 +165,21 @@ class DeviceBatch:
         # workspace=False: the caller passes one to launch() (shared / double-buffered)
         self.workspace = (torch.empty(self.workspace_bytes, dtype=torch.uint8, device=dev) if workspace
                           else None)
+        self._ws_done, self._ws_stream = None, None
 
-    def alloc_outputs(self, include_early: bool = True):
-        n = int(self.batch.total_out)
-        full = torch.empty(n, dtype=torch.float32, device=self.device)
-        early = torch.empty(n, dtype=torch.float32, device=self.device) if include_early else None
-        if self.pb.padded:
-            full.zero_()
-            if early is not None:
-                early.zero_()
-        direct = torch.empty(int(self.batch.total_channels), dtype=torch.int32, device=self.device)
+    def alloc_outputs(self, include_early: bool = True, stream=None):
+        """Output tensors, allocated (and, for padded layouts, zeroed) on
+        `stream` (default: current) so they are ordered with a launch there."""
+        st = torch.cuda.current_stream(self.device) if stream is None else stream
+        with torch.cuda.stream(st):
+            n = int(self.batch.total_out)
+            full = torch.empty(n, dtype=torch.float32, device=self.device)
+            early = torch.empty(n, dtype=torch.float32, device=self.device) if include_early else None
+            if self.pb.padded:
+                full.zero_()
+                if early is not None:
+                    early.zero_()
+            direct = torch.empty(int(self.batch.total_channels), dtype=torch.int32, device=self.device)
         return full, early, direct
 
     def launch(self, full, early, direct, stream=None, stages: int = _abi.STAGE_ALL, workspace=None) -> None:
@@ -184,15 +189,23 @@ class DeviceBatch:
         ws = self.workspace if workspace is None else workspace
         if ws is None or ws.numel() < self.workspace_bytes:
             raise ValueError(f"workspace too small: need {self.workspace_bytes} bytes")
+        own = workspace is None  # the batch's own workspace may be in use on another stream
+        if own and self._ws_done is not None and self._ws_stream != st:
+            st.wait_event(self._ws_done)
         status = _abi.lib().frir_simulate_stages(
             self.plan.handle, ctypes.byref(self.batch), ws.data_ptr(),
             ws.numel(), full.data_ptr(), early.data_ptr() if early is not None else None,
             direct.data_ptr(), st.cuda_stream, stages,
         )
         _abi.check(status, "frir_simulate_stages")
+        if own:
+            if self._ws_done is None:
+                self._ws_done = torch.cuda.Event()
+            self._ws_done.record(st)
+            self._ws_stream = st
 
     def run(self, include_early: bool = True, stream=None) -> BatchResult:
-        full, early, direct = self.alloc_outputs(include_early)
+        full, early, direct = self.alloc_outputs(include_early, stream)
         self.launch(full, early, direct, stream)
         return BatchResult(self.pb, full, early, direct)
 

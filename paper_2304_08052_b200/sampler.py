@@ -71,6 +71,7 @@ class DeviceSceneSampler:
         s.out_stride = self.out_stride
         self.cspec = s
         self.plan = engine.get_plan(spec.sample_rate, self.device)
+        self._ws, self._ws_done = None, None
         self.mics = torch.as_tensor(mics.reshape(-1), dtype=torch.float64, device=self.device)
 
     def jobs(self, seed: int, first: int, count: int, stream=None):
@@ -80,17 +81,20 @@ class DeviceSceneSampler:
         import torch
 
         n = count * self.S1
-        jobs = torch.empty(n * _abi.JOB_DTYPE.itemsize, dtype=torch.uint8, device=self.device)
-        chan_job = torch.empty(n * self.M, dtype=torch.int32, device=self.device)
-        status = torch.empty(count, dtype=torch.int32, device=self.device)
-        st = (torch.cuda.current_stream(self.device) if stream is None else stream).cuda_stream
-        _abi.check(_abi.lib().frir_sample_scene_jobs(self.plan.handle, ctypes.byref(self.cspec), int(seed),
-                                                    int(first), int(count), jobs.data_ptr(), chan_job.data_ptr(),
-                                                    status.data_ptr(), st), "frir_sample_scene_jobs")
-        bad = torch.nonzero(status).flatten()
-        if bad.numel():
-            i = int(bad[0])
-            raise ValueError(f"item {first + i}: {_STATUS.get(int(status[i]), 'invalid scene')}")
+        st = torch.cuda.current_stream(self.device) if stream is None else stream
+        # allocations and the status read run on `st`, ordered with the kernel
+        with torch.cuda.stream(st):
+            jobs = torch.empty(n * _abi.JOB_DTYPE.itemsize, dtype=torch.uint8, device=self.device)
+            chan_job = torch.empty(n * self.M, dtype=torch.int32, device=self.device)
+            status = torch.empty(count, dtype=torch.int32, device=self.device)
+            _abi.check(_abi.lib().frir_sample_scene_jobs(self.plan.handle, ctypes.byref(self.cspec), int(seed),
+                                                        int(first), int(count), jobs.data_ptr(),
+                                                        chan_job.data_ptr(), status.data_ptr(), st.cuda_stream),
+                       "frir_sample_scene_jobs")
+            bad = torch.nonzero(status).flatten()
+            if bad.numel():
+                i = int(bad[0])
+                raise ValueError(f"item {first + i}: {_STATUS.get(int(status[i]), 'invalid scene')}")
         return jobs, chan_job
 
     def render(self, seed: int, first: int, count: int, include_early: bool = True, stream=None):
@@ -117,16 +121,22 @@ class DeviceSceneSampler:
         b.max_windows = self.max_windows
         lib = _abi.lib()
         need = int(lib.frir_workspace_size(self.plan.handle, ctypes.byref(b)))
-        ws = getattr(self, "_ws", None)
-        if ws is None or ws.numel() < need:  # the workspace is reused across calls
-            ws = self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
-        full = torch.zeros(int(b.total_out), dtype=torch.float32, device=self.device)
-        early = torch.zeros_like(full) if include_early else None
-        direct = torch.empty(int(b.total_channels), dtype=torch.int32, device=self.device)
-        st = (torch.cuda.current_stream(self.device) if stream is None else stream).cuda_stream
-        _abi.check(lib.frir_simulate(self.plan.handle, ctypes.byref(b), ws.data_ptr(), ws.numel(),
-                                     full.data_ptr(), early.data_ptr() if early is not None else None,
-                                     direct.data_ptr(), st), "frir_simulate")
+        st = torch.cuda.current_stream(self.device) if stream is None else stream
+        with torch.cuda.stream(st):  # zero fills and outputs ordered with the render on `st`
+            ws = getattr(self, "_ws", None)
+            if ws is None or ws.numel() < need:
+                ws = self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            elif self._ws_done is not None:  # the reused workspace: wait for the last call's render
+                st.wait_event(self._ws_done)
+            full = torch.zeros(int(b.total_out), dtype=torch.float32, device=self.device)
+            early = torch.zeros_like(full) if include_early else None
+            direct = torch.empty(int(b.total_channels), dtype=torch.int32, device=self.device)
+            _abi.check(lib.frir_simulate(self.plan.handle, ctypes.byref(b), ws.data_ptr(), ws.numel(),
+                                         full.data_ptr(), early.data_ptr() if early is not None else None,
+                                         direct.data_ptr(), st.cuda_stream), "frir_simulate")
+            self._ws_done = torch.cuda.Event()
+            self._ws_done.record(st)
+            ws.record_stream(st)
         shape = (count, self.S1, self.M, self.out_stride)
         self._keep = (jobs, chan_job, ws)  # device tables stay alive until the launch is done
         return (full.view(shape), early.view(shape) if early is not None else None,

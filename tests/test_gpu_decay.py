@@ -81,3 +81,29 @@ def test_rendered_batch_t60_and_container(tmp_path):
         assert np.array_equal(recs[2 * j].samples, res.job_view(j, "full").cpu().numpy())
         assert np.array_equal(recs[2 * j + 1].samples, res.job_view(j, "early").cpu().numpy())
         assert recs[2 * j].seed == int(pj[j]["seed"]) and recs[2 * j + 1].kind == "early"
+
+
+def test_float64_rows_bit_identical_to_reference_arithmetic():
+    """FP64 input (e.g. the reference's own RIRs) stays FP64 end to end:
+    curve and T60 equal oracle/decay_port (the reference's numpy code) bit for
+    bit, including samples float32 cannot represent and tiny nonzero tails."""
+    from oracle import decay_port as O
+    from paper_2304_08052_b200 import decay as D
+
+    rng = np.random.default_rng(5)
+    n = 6000
+    t = np.arange(n) / 16000.0
+    for k in range(4):
+        h = rng.standard_normal(n) * np.exp(-6.9 * t / (0.2 + 0.2 * k))
+        h[-50:] *= 1e-60  # below float32's range: must not flush to zero
+        assert h.dtype == np.float64
+        c = D.schroeder_curve(h)
+        assert np.array_equal(c, O.schroeder(h)), k
+        got, ref = D.measure_t60(h, 16000), O.t60(h, 16000)
+        assert (math.isnan(got) and math.isnan(ref)) or got == pytest.approx(ref, rel=1e-12), k
+    # batch: float64 rows keep FP64, float32 rows give the float32 curve
+    h2 = np.stack([h, h * 0.5])
+    b = D.schroeder_batch(h2).cpu().numpy()
+    assert np.array_equal(b[0], O.schroeder(h)) and np.array_equal(b[1], O.schroeder(h * 0.5))
+    b32 = D.schroeder_batch(h2.astype(np.float32)).cpu().numpy()
+    assert np.array_equal(b32[0], O.schroeder(h.astype(np.float32).astype(np.float64)))
