@@ -2,6 +2,7 @@
 bench.py and reduce timings with MAX (no GPU needed)."""
 
 import hashlib
+import json
 import os
 import socket
 
@@ -92,3 +93,89 @@ def test_room_content_independent_of_sharding():
     a, b = workloads.config2(2), workloads.config2(4, start=2)
     assert np.array_equal(np.concatenate([a.jobs, b.jobs])["seed"], whole.jobs["seed"])
     assert np.array_equal(np.concatenate([a.jobs, b.jobs])["d0"], whole.jobs["d0"])
+
+
+# ---------------------------------------------------------------- bench.py's own launcher
+_RANK_PROBE = r'''
+import json, os, sys
+import torch, torch.distributed as dist
+dist.init_process_group("gloo")
+r, w = dist.get_rank(), dist.get_world_size()
+assert r == int(os.environ["RANK"]) == int(os.environ["LOCAL_RANK"]) and w == int(os.environ["WORLD_SIZE"])
+assert os.environ["MASTER_ADDR"] == "127.0.0.1"
+t = torch.tensor([10.0 + r], dtype=torch.float64)
+dist.all_reduce(t, op=dist.ReduceOp.MAX)
+n = torch.tensor([float(r + 1)], dtype=torch.float64)
+dist.all_reduce(n, op=dist.ReduceOp.SUM)
+if r == 0:
+    print(json.dumps({"world": w, "max_ms": float(t[0]), "sum": float(n[0])}), flush=True)
+dist.destroy_process_group()
+'''
+
+
+def test_launch_ranks_env_contract(tmp_path):
+    """bench.launch_ranks starts N processes with torchrun's env contract
+    (RANK/LOCAL_RANK/WORLD_SIZE, MASTER_ADDR=127.0.0.1, a free port); the
+    ranks rendezvous and reduce with MAX/SUM; only rank 0 prints."""
+    import subprocess
+    import sys
+
+    import bench
+
+    probe = tmp_path / "probe.py"
+    probe.write_text(_RANK_PROBE)
+    out = tmp_path / "out.txt"
+    with open(out, "w") as f:
+        code = subprocess.run([sys.executable, "-c",
+                               "import sys, bench; sys.exit(bench.launch_ranks(3, [sys.executable, %r]))" % str(probe)],
+                              cwd=str(bench.ROOT), stdout=f, timeout=120).returncode
+    assert code == 0
+    lines = [json.loads(x) for x in out.read_text().splitlines() if x.startswith("{")]
+    assert lines == [{"world": 3, "max_ms": 12.0, "sum": 6.0}]
+
+
+def test_launch_ranks_propagates_failure(tmp_path):
+    import sys
+
+    import bench
+
+    bad = tmp_path / "bad.py"
+    bad.write_text("import os, sys, time\nif os.environ['RANK'] == '1': sys.exit(3)\ntime.sleep(60)\n")
+    assert bench.launch_ranks(2, [sys.executable, str(bad)], timeout=90) == 3
+
+
+def test_bench_gpus_flag_spawns_ranks():
+    """`bench.py --gpus 2` without torchrun spawns the ranks itself; the
+    reference arm runs on rank 0 only and reports n_gpus = 2."""
+    import subprocess
+    import sys
+
+    import bench
+
+    res = subprocess.run([sys.executable, str(bench.ROOT / "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--config", "1", "--steps", "1", "--warmup", "1"],
+                         capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [json.loads(x) for x in res.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["impl"] == "reference"
+    assert lines[0]["config"]["rirs_per_step"] == 2 and lines[0]["value"] > 0
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_one_gpu_totals():
+    """The GPU arm through the launcher: 2 ranks (gloo, sharing one GPU) split
+    config 5's rooms; the line counts every rank's RIRs and says n_gpus 2."""
+    import subprocess
+    import sys
+
+    import bench
+
+    res = subprocess.run([sys.executable, str(bench.ROOT / "bench.py"), "--gpus", "2", "--dist-backend", "gloo",
+                          "--rooms", "2048", "--chunk", "512", "--steps", "3", "--warmup", "3", "--e2e-part", "512"],
+                         capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stderr[-3000:]
+    lines = [json.loads(x) for x in res.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["config"]["rirs_per_step"] == 2048
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["roofline"]["launches_per_step"] == 2
