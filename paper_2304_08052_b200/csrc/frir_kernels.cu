@@ -12,6 +12,8 @@
 //                     correction, coalesced full + early stores
 //                                                             resample.py:81-136
 // No atomics touch sample values, so outputs are bit-reproducible.
+#include <cstdlib>
+
 #include "frir_internal.h"
 #include "frir_philox.cuh"
 
@@ -388,6 +390,7 @@ struct SortArgs {
   SegWs sw;
   DevPlan plan;
   int r_h, t0;
+  int atom_ranks;  // 1: ranks from shared-memory atomics (see sort_kernel pass 2)
 };
 
 
@@ -500,8 +503,37 @@ __global__ void __launch_bounds__(NW * 32) sort_kernel(SortArgs A) {
   // pass 2: stable scatter, warp w walks its chunk in row order; early flags
   // (core.py:259-264) from the channel's direct arrival q0
   const int q0 = A.ws.chan_q0[c];
-  const int kbits = 32 - __clz(nbk + 31);  // bits of every key below nbk + 32
   int2 v = r_lo + lane < r_hi ? src[r_lo + lane] : make_int2(0, 0);
+  if (A.atom_ranks) {
+    // ranks from the shared-memory atomics: each item takes its bucket's
+    // next slot (row order within a warp instruction follows the hardware's
+    // lane-ascending service of conflicting atomics; tests compare this path
+    // bit for bit with the ballot path below)
+    for (int rb = r_lo; rb < r_hi; rb += 32) {
+      const int r = rb + lane;
+      const int2 cur = v;
+      if (r + 32 < r_hi) v = src[r + 32];  // prefetch the next row group
+      if (r < r_hi) {
+        int2 it = cur;
+        const int sp = (it.x & 0xFFFFF) - kSpBias - kExt;
+        const int phi = ((unsigned)it.x >> 20) & 0x3FF;
+        const int rel = A.r_h * sp - A.t0 - phi - q0;  // q - q0
+        if (rel >= -J.e_lo && rel <= J.e_hi) it.y ^= 0x80000000;  // early: negative gain
+        const int idx = ((it.x & 0xFFFFF) >> 5) * kSortWarps + warp;
+        int pos;
+        if constexpr (sizeof(CT) == 2) {
+          const unsigned sh = 16u * (idx & 1);
+          pos = (int)((atomicAdd(reinterpret_cast<unsigned*>(s_cnt) + (idx >> 1), 1u << sh) >> sh) & 0xFFFFu);
+        } else {
+          pos = (int)atomicAdd(reinterpret_cast<unsigned*>(s_cnt) + idx, 1u);
+        }
+        FRIR_CHECK(pos >= 0 && pos < rows);
+        dst[pos] = it;
+      }
+    }
+    return;
+  }
+  const int kbits = 32 - __clz(nbk + 31);  // bits of every key below nbk + 32
   for (int rb = r_lo; rb < r_hi; rb += 32) {
     const int r = rb + lane;
     const bool ok = r < r_hi;
@@ -1388,6 +1420,10 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_
       SortArgs sa;
       sa.jobs = b->jobs; sa.chan_job = b->chan_job; sa.ws = ws; sa.sw = sw;
       sa.r_h = d.r_h; sa.t0 = d.t0; sa.plan = plan->dev;
+      // ranks by shared-memory atomics (default) or by ballots (FRIR_SORT_BALLOT=1,
+      // the reference ordering the tests compare against bit for bit)
+      static const int ballot = getenv("FRIR_SORT_BALLOT") ? atoi(getenv("FRIR_SORT_BALLOT")) : 0;
+      sa.atom_ranks = ballot ? 0 : 1;
       const int nbk = ((b->max_windows * kWin + kSpBias) >> 5) + 3;
       if (sw.nextra) {
         e = cudaMemsetAsync(sw.nextra, 0, sizeof(int), st);

@@ -439,3 +439,33 @@ def test_segmented_channels_normalize_scales_seams():
             s = float(a[m] @ b[m]) / float(a[m] @ a[m])
             assert s > 0.1
             assert np.abs(b[m] - s * a[m]).max() <= 1e-6 * np.abs(b[m]).max(), (var, m)
+
+
+def test_sort_atomic_ranks_equal_ballot_ranks():
+    """K2 ranks items with shared-memory atomics; the ballot-per-key-bit path
+    (FRIR_SORT_BALLOT=1) is the explicitly stable reference ordering.  Both
+    must render the same bits (configs 2-5, incl. segmented 48 kHz rows)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    prog = (
+        "import hashlib, sys; sys.path.insert(0, %r)\n"
+        "import torch\n"
+        "from paper_2304_08052_b200 import engine, workloads\n"
+        "for cfg, rooms in ((2, 256), (3, 16), (4, 4), (5, 64)):\n"
+        "    w = workloads.build(cfg, rooms)\n"
+        "    if cfg == 4: w.jobs['n_images'][0] = 16384\n"
+        "    r = engine.simulate_jobs(w.sample_rate, w.jobs, w.mics)\n"
+        "    h = hashlib.sha256()\n"
+        "    for t in (r.full, r.early, r.direct_index): h.update(t.cpu().numpy().tobytes())\n"
+        "    print(cfg, h.hexdigest())\n" % str(root))
+    outs = []
+    for ballot in ("0", "1"):
+        env = dict(os.environ, FRIR_SORT_BALLOT=ballot)
+        res = subprocess.run([sys.executable, "-c", prog], env=env, capture_output=True, text=True, timeout=600)
+        assert res.returncode == 0, res.stderr[-2000:]
+        outs.append(res.stdout)
+    assert outs[0] == outs[1] and len(outs[0].splitlines()) == 4
