@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define FRIR_ABI_VERSION 2
+#define FRIR_ABI_VERSION 3
 
 enum {
   FRIR_OK = 0,
@@ -130,7 +130,11 @@ typedef struct {
    r^g / D with r = exp(-0.0805 V/S/t60) (ism.py:63-78) unless `reflection`
    > 0, and arrivals past the train end are dropped instead of clamped
    (ism.py:131-133).  Full variant only. */
-enum { FRIR_KIND_FRAM = 0, FRIR_KIND_ISM = 1 };
+/* FRIR_KIND_TRAIN: an explicit high-rate train (downsample_highpass_downsample
+   on a HighRateTrain or (M, L) array, resample.py:81-136) rendered by
+   frir_simulate_train; `duration` holds its length L in samples and
+   n_images + 1 the item slots per channel (frir_train_nonzeros). */
+enum { FRIR_KIND_FRAM = 0, FRIR_KIND_ISM = 1, FRIR_KIND_TRAIN = 2 };
 
 typedef struct {
   const frir_job* jobs;      /* device, n_jobs entries */
@@ -297,6 +301,61 @@ int frir_edc_f64(const double* h, int64_t ld, const int32_t* len, int32_t C, dou
 int frir_t60_f64(const double* h, int64_t ld, const int32_t* len, int32_t C, const double* edc, int64_t ld_e,
                  const double* amax, double sample_rate, double max_drop, double floor_margin, double min_drop,
                  double* t60, void* stream);
+
+/* ---- stage API (reference framrir/__init__.py:15-28) ---------------------
+   Device forms of the reference's public stage functions, for callers that
+   use them one by one; the batched hot path above never materialises these
+   intermediates.  All buffers are device memory, FP64 in numpy's operation
+   order, asynchronous on `stream`. */
+
+/* Elementwise stage arithmetic.  params[0..3] per op:
+   FRIR_STAGE_RATIO_SAMPLE  quadratic_ratio_sample (core.py:94-100) from the
+                            uniform draws x0: {alpha**3, beta**3, -, -}
+   FRIR_STAGE_RESCALE       rescale_distance_ratio (core.py:103-110) of x0:
+                            {alpha, beta, max_ratio, -}
+   FRIR_STAGE_REFLECTIONS   sample_reflection_counts (core.py:213-220): x0 = D,
+                            x1 = DR, x2 = perturbation p: {c0*t60, rr_max, tau, -} */
+#define FRIR_STAGE_RATIO_SAMPLE 0
+#define FRIR_STAGE_RESCALE 1
+#define FRIR_STAGE_REFLECTIONS 2
+int frir_stage_eval(int32_t op, const double* x0, const double* x1, const double* x2, int64_t n,
+                    const double* params /* host, 4 */, double* out, void* stream);
+/* Generator(Philox(SeedSequence((seed, k, stage)))).uniform(lo, hi) words
+   [first_word, first_word + n) on the device (core.py:86-91, :215). */
+int frir_philox_uniform(uint64_t seed, uint64_t source_index, uint64_t stage, int64_t first_word, int64_t n,
+                        double lo, double hi, double* out, void* stream);
+/* sample_image_geometry (core.py:131-183) for every (native-draw) job of the
+   batch: ImageSet rows at img_off + i (i = 0 the direct path), per-mic
+   distances row-major at item_off + i * n_mics + m; reflection counts from
+   the stage-1 stream when with_reflections, else NaN (rows >= 1) as the
+   reference leaves them. */
+int frir_image_set(const frir_plan* plan, const frir_batch* batch, double* distances, double* azimuths,
+                   double* elevations, double* distance_ratios, double* reflections, double* mic_distances,
+                   int32_t with_reflections, void* stream);
+/* build_impulse_train (core.py:228-251): q = min(ceil(D / c0 * rate), L - 1)
+   (int32, rows x n_mics) and the dense (n_mics, L) FP64 train, colliding
+   arrivals summed in row order like np.add.at.  scratch: device bytes >=
+   frir_impulse_train_scratch(). */
+int64_t frir_impulse_train_scratch(int32_t rows, int32_t n_mics, int32_t length);
+int frir_impulse_train(const double* mic_distances, const double* reflections, int32_t rows, int32_t n_mics,
+                       double r, double sound_speed, int64_t rate, int32_t length, double* train, int32_t* q,
+                       void* scratch, int64_t scratch_bytes, void* stream);
+/* early_reverb_train (core.py:254-265): out = train where
+   -lo <= n - q0[m] <= hi, else 0. */
+int frir_early_window(const double* train, int32_t n_mics, int64_t length, const int32_t* q0, int64_t lo,
+                      int64_t hi, double* out, void* stream);
+/* downsample_highpass_downsample (resample.py:81-136) of explicit trains:
+   frir_train_nonzeros counts the samples with sign * x > 0 per row (the item
+   slots a FRIR_KIND_TRAIN job needs); frir_simulate_train renders the full
+   variant of every job's rows (channel c = row c of `train`, stride ld) from
+   those samples through the same sort / tail / render kernels as
+   frir_simulate.  A train with negative samples is rendered as sign +1 minus
+   sign -1. */
+int frir_train_nonzeros(const double* train, int64_t ld, int32_t rows, int32_t length, int32_t sign,
+                        int32_t* counts, void* stream);
+int frir_simulate_train(const frir_plan* plan, const frir_batch* batch, void* workspace, size_t workspace_bytes,
+                        const double* train, int64_t ld, int32_t sign, float* out_full, int32_t* direct_scratch,
+                        void* stream);
 
 const char* frir_last_error(void);
 int32_t frir_abi_version(void);

@@ -82,8 +82,9 @@ JOB_DTYPE = np.dtype(FrirJob)
 
 # (name, restype, argtypes) of every symbol include/frir.h declares.
 MIX_POWER_CHUNKS = 32  # FRIR_MIX_POWER_CHUNKS
-ABI_VERSION = 2  # FRIR_ABI_VERSION
-KIND_FRAM, KIND_ISM = 0, 1  # FRIR_KIND_*
+ABI_VERSION = 3  # FRIR_ABI_VERSION
+KIND_FRAM, KIND_ISM, KIND_TRAIN = 0, 1, 2  # FRIR_KIND_*
+STAGE_RATIO_SAMPLE, STAGE_RESCALE, STAGE_REFLECTIONS = 0, 1, 2  # frir_stage_eval ops
 
 SIGNATURES = [
     ("frir_plan_create", c_int32, [c_int32, ctypes.POINTER(c_void_p)]),
@@ -124,6 +125,21 @@ SIGNATURES = [
     ("frir_t60_f64", c_int32,
      [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_int64, c_void_p, c_double, c_double, c_double,
       c_double, c_void_p, c_void_p]),
+    ("frir_stage_eval", c_int32, [c_int32, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    ("frir_philox_uniform", c_int32,
+     [c_uint64, c_uint64, c_uint64, c_int64, c_int64, c_double, c_double, c_void_p, c_void_p]),
+    ("frir_image_set", c_int32,
+     [c_void_p, ctypes.POINTER(FrirBatch), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32,
+      c_void_p]),
+    ("frir_impulse_train_scratch", c_int64, [c_int32, c_int32, c_int32]),
+    ("frir_impulse_train", c_int32,
+     [c_void_p, c_void_p, c_int32, c_int32, c_double, c_double, c_int64, c_int32, c_void_p, c_void_p, c_void_p,
+      c_int64, c_void_p]),
+    ("frir_early_window", c_int32, [c_void_p, c_int32, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
+    ("frir_train_nonzeros", c_int32, [c_void_p, c_int64, c_int32, c_int32, c_int32, c_void_p, c_void_p]),
+    ("frir_simulate_train", c_int32,
+     [c_void_p, ctypes.POINTER(FrirBatch), c_void_p, ctypes.c_size_t, c_void_p, c_int64, c_int32, c_void_p, c_void_p,
+      c_void_p]),
     ("frir_last_error", ctypes.c_char_p, []),
     ("frir_abi_version", c_int32, []),
     ("frir_struct_size", c_int64, [c_int32]),

@@ -11,7 +11,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT = PKG / "lib" / "libfrir.so"
-SOURCES = ["frir_abi.cu", "frir_kernels.cu", "frir_mix.cu", "frir_fftconv.cu", "frir_decay.cu", "frir_scene.cu", "frir_design.cpp"]
+SOURCES = ["frir_abi.cu", "frir_kernels.cu", "frir_mix.cu", "frir_fftconv.cu", "frir_decay.cu", "frir_scene.cu", "frir_stages.cu", "frir_design.cpp"]
 HEADERS = ["frir_internal.h", "frir_design.h", "frir_philox.cuh"]
 INCLUDE = PKG.parent / "include" / "frir.h"
 

@@ -49,3 +49,21 @@ def config_scene(cfg: dict) -> Scene:
     if "mic_spacings" in section:
         section["mic_positions"] = linear_array(section.pop("mic_spacings"))
     return Scene(**section)
+
+
+def config_mixture_spec(cfg: dict):
+    """MixtureSpec from the "mixture" section, lists as tuples (io.py:163-168)."""
+    from .mixture import MixtureSpec
+
+    section = {k: tuple(v) if isinstance(v, list) else v for k, v in cfg.get("mixture", {}).items()}
+    return MixtureSpec(**section)
+
+
+def config_curriculum(cfg: dict):
+    """CurriculumState from the "curriculum" section, or None (io.py:171-174)."""
+    if "curriculum" not in cfg:
+        return None
+    from .mixture import CurriculumState
+
+    return CurriculumState(**cfg["curriculum"])
+

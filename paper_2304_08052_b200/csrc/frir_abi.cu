@@ -221,12 +221,24 @@ int frir_jobs_prepare(int32_t sample_rate, frir_job* jobs, int32_t n_jobs, int32
   for (int32_t j = 0; j < n_jobs; ++j) {
     frir_job& J = jobs[j];
     std::string pre = "job " + std::to_string(j) + ": ";
-    if (J.kind != FRIR_KIND_FRAM && J.kind != FRIR_KIND_ISM) {
+    if (J.kind != FRIR_KIND_FRAM && J.kind != FRIR_KIND_ISM && J.kind != FRIR_KIND_TRAIN) {
       set_error(pre + "unknown job kind " + std::to_string(J.kind));
       return FRIR_EINVAL;
     }
     const bool ism = J.kind == FRIR_KIND_ISM;
-    if (ism) {
+    const bool train = J.kind == FRIR_KIND_TRAIN;
+    if (train) {
+      // an explicit high-rate train of `duration` samples (frir_simulate_train)
+      if (!(J.duration >= 1.0 && J.duration == std::floor(J.duration))) {
+        set_error(pre + "a train job needs its length in samples as duration");
+        return FRIR_EINVAL;
+      }
+      if (J.n_mics < 1 || J.n_images < 0) { set_error(pre + "a train job needs rows and channels"); return FRIR_EINVAL; }
+      J.t60 = 1.0;
+      J.r = 0.5;
+      J.rr_max = 0.0;
+      J.normalize = 0;
+    } else if (ism) {
       // IsmConfig / ism_rir (ism.py:39-60, 63-78, 118-126); positions come as draws
       if (!(J.t60 > 0)) { set_error(pre + "t60 must be > 0"); return FRIR_EINVAL; }
       if (!(J.c0 > 0)) { set_error(pre + "sound_speed must be > 0"); return FRIR_EINVAL; }
@@ -330,7 +342,7 @@ int frir_jobs_prepare(int32_t sample_rate, frir_job* jobs, int32_t n_jobs, int32
     seed_keys(J.seed, (uint64_t)J.source_index, 1, key);
     J.key[2] = key[0]; J.key[3] = key[1];
     // lengths (core.py:239, scipy resample_poly output lengths)
-    double Ld = std::ceil((ism && J.duration > 0 ? J.duration : J.t60) * (double)rate);
+    double Ld = train ? J.duration : std::ceil((ism && J.duration > 0 ? J.duration : J.t60) * (double)rate);
     if (!(Ld >= 1.0 && Ld < 2.0e9)) { set_error(pre + "RIR length out of range"); return FRIR_ERANGE; }
     J.L = (int32_t)Ld;
     int64_t n1 = ceil_div64((int64_t)J.L * d.up, d.down);

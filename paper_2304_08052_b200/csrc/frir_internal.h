@@ -78,5 +78,12 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* ws, size_t
 size_t workspace_bytes(const frir_batch* b);
 int launches(const frir_batch* b, int early);
 cudaError_t init_launch_cache(frir_plan* plan);
+int launch_image_set(const frir_plan* plan, const frir_batch* b, double* dist, double* az, double* el,
+                     double* ratio, double* refl, double* mic_dist, int with_refl, cudaStream_t st);
+int train_nonzeros(const double* train, int64_t ld, int32_t rows, int32_t L, int32_t sign, int32_t* counts,
+                   cudaStream_t st);
+int launch_simulate_train(const frir_plan* plan, const frir_batch* b, void* ws, size_t ws_bytes,
+                          const double* train, int64_t ld, int32_t sign, float* out_full, int32_t* direct_scratch,
+                          cudaStream_t st);
 int check_line();
 }  // namespace frir

@@ -203,8 +203,14 @@ __device__ __forceinline__ int2 make_item(int q, float a, int r_h, int t0, unsig
 // Per-image part of K1 for images 4g + 1 .. 4g + 4 of job J: absolute image
 // positions (FP64, numpy's operation order) and the FP32 gains r^g.  Shared by
 // geom_kernel and image_kernel.
+// The sampled ImageSet fields of the 4 images (core.py:43-62), for image_set_kernel.
+struct ImageDraws {
+  double dist[4], az[4], el[4], ratio[4], refl[4];
+};
+
 __device__ __forceinline__ void image_group(const GeomArgs& A, const frir_job& J, int g, double (&px)[4],
-                                            double (&py)[4], double (&pz)[4], float (&lg)[4]) {
+                                            double (&py)[4], double (&pz)[4], float (&lg)[4],
+                                            ImageDraws* draws = nullptr) {
   const int I = J.n_images;
   const int ism = J.kind == FRIR_KIND_ISM;
   const double c_max = __dmul_rn(J.c0, J.t60);
@@ -275,6 +281,13 @@ __device__ __forceinline__ void image_group(const GeomArgs& A, const frir_job& J
       gg = fmin(fmax(gg, 1.0), J.rr_max);
       dist[k] = dd;
       refl[k] = gg;
+      if (draws) draws->ratio[k] = dr;
+    }
+  }
+  if (draws) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      draws->dist[k] = dist[k]; draws->az[k] = th[k]; draws->el[k] = ph[k]; draws->refl[k] = refl[k];
     }
   }
 #pragma unroll
@@ -1282,6 +1295,114 @@ __global__ void __launch_bounds__(256) seam_kernel(const __grid_constant__ SeamA
   }
 }
 
+// ---------------------------------------------------------------- stage API kernels
+// sample_image_geometry (core.py:131-183) for every job of a native-draw
+// batch: the ImageSet rows K1 renders from -- distances, azimuths,
+// elevations, distance ratios at img_off + i, per-mic distances at
+// item_off + i * M + m (row-major (I + 1, M) like the reference), and, when
+// `with_refl`, the reflection counts of sample_reflection_counts (core.py:
+// 195-221) from the stage-1 stream (else NaN, as the reference leaves them).
+struct ImageSetOut {
+  double *dist, *az, *el, *ratio, *refl, *mic_dist;
+  int with_refl;
+};
+
+__global__ void __launch_bounds__(128) image_set_kernel(GeomArgs A, ImageSetOut O) {
+  const int j = blockIdx.x;
+  const frir_job& J = A.jobs[j];
+  const int I = J.n_images, M = J.n_mics;
+  const int g = blockIdx.y * blockDim.x + threadIdx.x;
+  const double* mics = A.mics + 3 * (size_t)J.mic_off;
+  const double nan = __longlong_as_double(0x7ff8000000000000ll);
+  auto mic_row = [&](size_t i, double x, double y, double z) {  // params.py:162-171 distances_to_mics
+    for (int m = 0; m < M; ++m) {
+      const double dx = __dsub_rn(x, mics[3 * m]), dy = __dsub_rn(y, mics[3 * m + 1]), dz = __dsub_rn(z, mics[3 * m + 2]);
+      O.mic_dist[J.item_off + i * M + m] =
+          __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+    }
+  };
+  if (g == 0) {  // row 0: the direct path (core.py:163-169)
+    double x, y, z;
+    image_position(J, J.d0, J.az, J.el, &x, &y, &z);
+    const size_t o = J.img_off;
+    O.dist[o] = J.d0; O.az[o] = J.az; O.el[o] = J.el; O.ratio[o] = 1.0; O.refl[o] = 0.0;
+    mic_row(0, x, y, z);
+  }
+  if (g >= (I + 3) / 4) return;
+  double px[4], py[4], pz[4];
+  float lg[4];
+  ImageDraws d;
+  image_group(A, J, g, px, py, pz, lg, &d);
+  const int nk = min(4, I - 4 * g);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (k >= nk) break;
+    const size_t i = 4 * (size_t)g + k + 1, o = J.img_off + i;
+    O.dist[o] = d.dist[k]; O.az[o] = d.az[k]; O.el[o] = d.el[k]; O.ratio[o] = d.ratio[k];
+    O.refl[o] = O.with_refl ? d.refl[k] : nan;
+    mic_row(i, px[k], py[k], pz[k]);
+  }
+}
+
+// Sparse items of explicit high-rate trains (downsample_highpass_downsample
+// on a HighRateTrain or (M, L) array, resample.py:81-136): channel c of the
+// batch is row c of `train`; its samples with sign * x > 0 become items
+// (index n, amplitude sign * x[n]) in index order, the rest of the row's item
+// slots go to the dropped bucket.  One CTA per channel, ordered compaction.
+constexpr int kTrainThreads = 256;
+__global__ void __launch_bounds__(kTrainThreads) train_items_kernel(const double* __restrict__ train, long ld,
+                                                                     int sign, const frir_job* jobs,
+                                                                     const int32_t* chan_job, Workspace ws, int r_h,
+                                                                     int t0, unsigned magic) {
+  __shared__ int s_w[kTrainThreads / 32];
+  __shared__ int s_base;
+  const int c = blockIdx.x;
+  const frir_job& J = jobs[chan_job[c]];
+  const int m = c - J.chan_off, rows = J.n_images + 1, L = J.L;
+  const double* x = train + (size_t)c * ld;
+  int2* out = ws.items_raw + J.item_off + (size_t)m * rows;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    s_base = 0;
+    ws.chan_q0[c] = 0;
+    ws.chan_scale[c] = 1.0f;
+  }
+  __syncthreads();
+  for (int n0 = 0; n0 < L; n0 += kTrainThreads) {
+    const int n = n0 + threadIdx.x;
+    const double v = n < L ? sign * x[n] : 0.0;
+    const bool keep = v > 0.0;
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) s_w[warp] = __popc(bal);
+    __syncthreads();
+    int off = s_base;
+    for (int w2 = 0; w2 < warp; ++w2) off += s_w[w2];
+    if (keep) {
+      const int pos = off + __popc(bal & ((1u << lane) - 1u));
+      FRIR_CHECK(pos < rows);
+      out[pos] = make_item(n, (float)v, r_h, t0, magic);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int w2 = 0; w2 < kTrainThreads / 32; ++w2) t += s_w[w2];
+      s_base += t;
+    }
+    __syncthreads();
+  }
+  for (int p = s_base + threadIdx.x; p < rows; p += kTrainThreads) out[p] = dropped_item(J.n2);
+}
+
+// Nonzeros with sign * x > 0 per row (the item count of train_items_kernel).
+__global__ void __launch_bounds__(kTrainThreads) train_count_kernel(const double* __restrict__ train, long ld, int L,
+                                                                     int sign, int32_t* counts) {
+  const double* x = train + (size_t)blockIdx.x * ld;
+  int n = 0;
+  for (int i = threadIdx.x; i < L; i += kTrainThreads) n += sign * x[i] > 0.0;
+  for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+  if ((threadIdx.x & 31) == 0 && n) atomicAdd(counts + blockIdx.x, n);
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- host launcher
@@ -1490,6 +1611,62 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_
     }
   }
   return FRIR_OK;
+}
+
+
+static GeomArgs geom_args(const frir_plan* plan, const frir_batch* b, Workspace ws, int32_t* direct_index) {
+  const frir_plan_desc& d = plan->dev.d;
+  GeomArgs ga;
+  ga.jobs = b->jobs; ga.mics = b->mics;
+  ga.draw_dist = b->draw_dist; ga.draw_az = b->draw_az; ga.draw_el = b->draw_el; ga.draw_refl = b->draw_refl;
+  ga.ws = ws; ga.direct_index = direct_index;
+  ga.r_h = d.r_h; ga.t0 = d.t0;
+  ga.rh_magic = (unsigned)((0x100000000ull + d.r_h - 1) / d.r_h);
+  ga.rate = (double)d.r_h * d.sample_rate;
+  return ga;
+}
+
+int launch_image_set(const frir_plan* plan, const frir_batch* b, double* dist, double* az, double* el,
+                     double* ratio, double* refl, double* mic_dist, int with_refl, cudaStream_t st) {
+  if (b->n_jobs == 0) return FRIR_OK;
+  Workspace ws{};
+  GeomArgs ga = geom_args(plan, b, ws, nullptr);
+  ImageSetOut o{dist, az, el, ratio, refl, mic_dist, with_refl};
+  const int maxg = (b->max_rows - 1 + 3) / 4;
+  image_set_kernel<<<dim3(b->n_jobs, maxg > 0 ? (maxg + 127) / 128 : 1), 128, 0, st>>>(ga, o);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { set_error(std::string("image_set_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
+  return FRIR_OK;
+}
+
+int train_nonzeros(const double* train, int64_t ld, int32_t rows, int32_t L, int32_t sign, int32_t* counts,
+                   cudaStream_t st) {
+  if (rows <= 0) return FRIR_OK;
+  cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(int32_t) * rows, st);
+  if (e == cudaSuccess) {
+    train_count_kernel<<<rows, kTrainThreads, 0, st>>>(train, (long)ld, L, sign, counts);
+    e = cudaGetLastError();
+  }
+  if (e != cudaSuccess) { set_error(std::string("train_count_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
+  return FRIR_OK;
+}
+
+int launch_simulate_train(const frir_plan* plan, const frir_batch* b, void* wsp, size_t ws_bytes,
+                          const double* train, int64_t ld, int32_t sign, float* out_full, int32_t* direct_scratch,
+                          cudaStream_t st) {
+  if (ws_bytes < workspace_bytes(b)) {
+    set_error("workspace too small: need " + std::to_string(workspace_bytes(b)) + " bytes");
+    return FRIR_ENOMEM;
+  }
+  if (b->n_jobs == 0 || b->total_channels == 0) return FRIR_OK;
+  const Workspace ws = carve(wsp, b);
+  const GeomArgs ga = geom_args(plan, b, ws, direct_scratch);
+  train_items_kernel<<<b->total_channels, kTrainThreads, 0, st>>>(train, (long)ld, sign, b->jobs, b->chan_job, ws,
+                                                                   ga.r_h, ga.t0, ga.rh_magic);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { set_error(std::string("train_items_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
+  return launch_simulate(plan, b, wsp, ws_bytes, out_full, nullptr, direct_scratch, st,
+                         FRIR_STAGE_DELAY | FRIR_STAGE_RENDER);
 }
 
 }  // namespace frir

@@ -111,6 +111,50 @@ class SyntheticPool:
         return x / peak if peak > 0 else x
 
 
+@dataclass
+class WavDirectoryPool:
+    """Clean mono WAV files from a user-supplied directory (mixture.py:143-168):
+    a file and a start drawn from the caller's rng in the reference's order;
+    integer PCM normalised by its type range (io.py:39-55).  Source material
+    I/O on the host, like the reference's."""
+
+    directory: str
+
+    def _files(self):
+        import pathlib
+
+        files = sorted(pathlib.Path(self.directory).glob("*.wav"))
+        if not files:
+            raise ValueError(f"no .wav files under {self.directory}")
+        return files
+
+    @staticmethod
+    def _read(path):
+        from scipy.io import wavfile
+
+        fs, data = wavfile.read(path)
+        scale = {np.dtype(np.int16): 32768.0, np.dtype(np.int32): 2147483648.0}.get(data.dtype)
+        if scale is not None:
+            data = data / scale
+        elif data.dtype == np.uint8:
+            data = (data.astype(float) - 128.0) / 128.0
+        else:
+            data = data.astype(np.float64)
+        return (data[None, :] if data.ndim == 1 else data.T), int(fs)
+
+    def draw(self, rng, n_samples: int, sample_rate: int) -> np.ndarray:
+        files = self._files()
+        x, fs = self._read(files[int(rng.integers(len(files)))])
+        if fs != sample_rate:
+            raise ValueError(f"expected {sample_rate} Hz material, got {fs} Hz")
+        x = x[0] if x.ndim == 2 else x
+        if len(x) >= n_samples:
+            start = int(rng.integers(len(x) - n_samples + 1))
+            return x[start: start + n_samples]
+        reps = int(np.ceil(n_samples / len(x)))
+        return np.tile(x, reps)[:n_samples]
+
+
 def sample_scene(spec: MixtureSpec, rng, curriculum: CurriculumState | None = None) -> tuple:
     """One utterance's (Scene, SimParams), drawing from ``rng`` in the
     reference's order (mixture.py:171-213): room (3 uniforms), T60, then per

@@ -139,3 +139,55 @@ def test_product_never_imports_oracle():
     for f in pkg.rglob("*.py"):
         text = f.read_text()
         assert "from oracle" not in text and "import oracle" not in text, f
+
+
+# The reference's public names (framrir/__init__.py:43-83, framrir_binding/__init__.py:35-42):
+REFERENCE_ALL = [
+    "__version__", "SimParams", "Scene", "linear_array", "array_center", "source_position", "sph_to_cart",
+    "ImageSet", "HighRateTrain", "RirResult", "RirFilter", "RateFactors", "quadratic_ratio_sample",
+    "rescale_distance_ratio", "reflection_coefficient", "sample_image_geometry", "max_reflections",
+    "sample_reflection_counts", "build_impulse_train", "early_reverb_train", "simulate_rir", "rate_factors",
+    "downsample_highpass_downsample", "IsmConfig", "enumerate_images", "eyring_reflection_coefficient", "ism_rir",
+    "schroeder_curve", "measure_t60", "MixtureSpec", "MixtureResult", "CurriculumState", "SyntheticPool",
+    "WavDirectoryPool", "sample_scene", "spatialize_and_mix", "curriculum_step", "generate_batch",
+]
+BINDING_ALL = ["__version__", "__core_version__", "BindingError", "BindingBatch", "py_simulate_rir",
+               "py_generate_batch"]
+
+
+def test_every_reference_name_is_exported():
+    import paper_2304_08052_b200 as F
+    from paper_2304_08052_b200 import binding
+
+    assert [n for n in REFERENCE_ALL if not hasattr(F, n)] == []
+    assert [n for n in BINDING_ALL if not hasattr(binding, n)] == []
+    assert set(REFERENCE_ALL) <= set(F.__all__)
+
+
+def test_stage_dataclasses_and_binding_batch():
+    import numpy as np
+
+    import paper_2304_08052_b200 as F
+
+    im = F.ImageSet(distances=np.array([1.0, 2.0, 3.0]), azimuths=np.zeros(3), elevations=np.zeros(3),
+                    distance_ratios=np.array([1.0, 2.0, 3.0]), mic_distances=np.ones((3, 2)),
+                    reflections=np.zeros(3), direct_distance=1.0)
+    assert im.n_images == 2 and np.array_equal(im.direct_mic_distances, [1.0, 1.0])
+    tr = F.HighRateTrain(channels=np.zeros((2, 7)), direct_index=np.array([1, 2]), rate=992000)
+    assert tr.length == 7
+    b = F.BindingBatch()
+    assert len(b) == 0 and b.metadata == []
+    with pytest.raises(NotImplementedError):
+        F.downsample_highpass_downsample(tr, F.rate_factors(16000), highpass_hz=100.0)
+
+
+def test_config_mixture_sections():
+    from paper_2304_08052_b200 import config
+
+    cfg = config.validate_config({"mixture": {"n_speakers": 1, "t60_range": [0.2, 0.4]},
+                                  "curriculum": {"epoch": 0}})
+    spec = config.config_mixture_spec(cfg)
+    assert spec.n_speakers == 1 and spec.t60_range == (0.2, 0.4)
+    assert config.config_curriculum(cfg).epoch == 0 and config.config_curriculum({}) is None
+    with pytest.raises(ValueError):
+        config.validate_config({"mixture": {"bogus": 1}})
