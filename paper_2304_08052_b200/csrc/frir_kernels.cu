@@ -304,8 +304,11 @@ __device__ __forceinline__ void image_group(const GeomArgs& A, const frir_job& J
 }
 
 #ifndef FRIR_GEOM_MINB
-#define FRIR_GEOM_MINB 8
+#define FRIR_GEOM_MINB 6  // 85 registers: fewer spills in the FP64 + Philox code than at 8 (measured)
 #endif
+// geom_kernel's per-warp transpose rows: 36 entries of 8 bytes keep both the
+// row writes and the column reads free of bank conflicts
+constexpr int kTrStride = 36;
 // Buckets of a channel's items (32-sample output windows, biased) and the
 // extra bucket after them that holds ISM arrivals past the train end
 // (ism.py:131-133 drops them): the sort puts them last and K2b / K3 stop
@@ -341,27 +344,47 @@ __global__ void __launch_bounds__(128, FRIR_GEOM_MINB) geom_kernel(GeomArgs A) {
       A.direct_index[J.chan_off + m] = di < 0 ? 0 : (di > J.n2 - 1 ? J.n2 - 1 : di);
     }
   }
-  if (g >= ngroups) return;
+  // Lanes own 4 consecutive rows; per mic the warp's 128 items go through a
+  // padded shared-memory transpose so each store writes 32 consecutive rows
+  // (coalesced 256-byte stores instead of 8-byte writes at a 32-byte stride).
+  const int lane = threadIdx.x & 31;
+  const bool live = g < ngroups;
+  if (!__any_sync(0xffffffffu, live)) return;
+  __shared__ int2 s_tr[128 / 32][4 * kTrStride];
+  int2* tr = s_tr[threadIdx.x >> 5];
   double px[4], py[4], pz[4];
   float lg[4];
-  image_group(A, J, g, px, py, pz, lg);
-  const int r0 = 4 * g + 1;
-  const int nk = min(4, I - 4 * g);
+  if (live) {
+    image_group(A, J, g, px, py, pz, lg);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { px[k] = py[k] = pz[k] = 1.0; lg[k] = 0.f; }
+  }
+  const int nk = live ? min(4, I - 4 * g) : 0;
+  const int wrow = 4 * (g - lane) + 1;  // first row of the warp
   for (int m = 0; m < M; ++m) {
-    int2* out = items + (size_t)m * rows + r0;
+    int2* out = items + (size_t)m * rows + wrow;
     const double mx = __ldg(mics + 3 * m), my = __ldg(mics + 3 * m + 1), mz = __ldg(mics + 3 * m + 2);
+    int2 it[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
+      it[k] = make_int2(0, 0);
       if (k < nk) {
         float inv_d;
         const int q = delay_fast(px[k], py[k], pz[k], mx, my, mz, J.c0, A.rate, rate_c0, J.L + ism, &inv_d);
-        if (q > J.L - 1) {  // ISM only: dropped arrival
-          out[k] = dropped_item(J.n2);
-          continue;
-        }
-        FRIR_CHECK(q >= 0 && q < J.L && r0 + k < rows);
-        out[k] = make_item(q, lg[k] * inv_d, A.r_h, A.t0, A.rh_magic);  // r^g / D
+        FRIR_CHECK(q >= 0 && q < J.L + ism && 4 * g + 1 + k < rows);
+        it[k] = q > J.L - 1 ? dropped_item(J.n2)  // ISM only: dropped arrival
+                            : make_item(q, lg[k] * inv_d, A.r_h, A.t0, A.rh_magic);  // r^g / D
       }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) tr[k * kTrStride + lane] = it[k];  // item 4 lane + k
+    __syncwarp();
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {  // rows 32 kk + lane of the warp
+      const int row = 32 * kk + lane;
+      if (wrow + row <= I) out[row] = tr[(lane & 3) * kTrStride + 8 * kk + (lane >> 2)];
     }
   }
 }
