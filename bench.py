@@ -184,8 +184,8 @@ def cpu_rate(cfg: int, n_jobs: int, workers: int, repeats: int = 1, warmup: int 
     jobs = cpu_jobs(cfg, n_jobs)
     walls = []
     with ProcessPoolExecutor(max_workers=workers) as ex:
-        for _ in range(max(1, warmup)):
-            list(ex.map(fn, jobs[:workers]))
+        for _ in range(max(1, warmup)):  # every worker imports numpy/scipy and runs one job first
+            list(ex.map(fn, [jobs[i % len(jobs)] for i in range(workers)]))
         for _ in range(repeats):
             t0 = time.perf_counter()
             list(ex.map(fn, jobs))
