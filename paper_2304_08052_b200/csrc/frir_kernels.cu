@@ -427,6 +427,8 @@ struct SortArgs {
   DevPlan plan;
   int r_h, t0;
   int atom_ranks;  // 1: ranks from shared-memory atomics (see sort_kernel pass 2)
+  int stage_off;   // > 0: byte offset of a max_rows-item shared-memory buffer the
+                   // scatter writes first (then copied out coalesced); 0: scatter to HBM
 };
 
 
@@ -459,6 +461,7 @@ __global__ void __launch_bounds__(NW * 32) sort_kernel(SortArgs A) {
   const int2* src = A.ws.items_raw + base;
   int2* dst = A.ws.items + base;
   CT* s_cnt = reinterpret_cast<CT*>(smem);  // [nbk][warps]
+  int2* s_sorted = A.stage_off ? reinterpret_cast<int2*>(smem + A.stage_off) : nullptr;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = nbk * kSortWarps;
   const int nwords = (int)((n * sizeof(CT) + 3) / 4);
@@ -564,8 +567,13 @@ __global__ void __launch_bounds__(NW * 32) sort_kernel(SortArgs A) {
           pos = (int)atomicAdd(reinterpret_cast<unsigned*>(s_cnt) + idx, 1u);
         }
         FRIR_CHECK(pos >= 0 && pos < rows);
-        dst[pos] = it;
+        if (s_sorted) s_sorted[pos] = it;
+        else dst[pos] = it;
       }
+    }
+    if (s_sorted) {  // the sorted row leaves shared memory in coalesced stores
+      __syncthreads();
+      for (int i = tid; i < rows; i += kSortThreads) dst[i] = s_sorted[i];
     }
     return;
   }
@@ -1447,6 +1455,7 @@ size_t workspace_bytes(const frir_batch* b) {
 
 static int table_blocks(const frir_plan_desc& d) { return (d.sup + 31) / 32; }
 constexpr int kDynSlack = 1024;  // >= any kernel's static smem; launches check sizes against optin - slack
+constexpr int kSortStageRows = 4608;  // sorted rows staged in shared memory up to this length (measured: helps config 2, not config 5)
 
 static size_t render_smem(const frir_plan_desc& d, bool early) {
   const int v = early ? 2 : 1;
@@ -1586,6 +1595,15 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_
         set_error("RIR too long for the per-channel sort: " + std::to_string(nbk) + " buckets need " +
                   std::to_string(smem) + " bytes of shared memory");
         return FRIR_ERANGE;
+      }
+      // short rows: the scatter goes to shared memory first (<= 36 KB) and the
+      // sorted row leaves in coalesced stores (longer rows: the buffer costs
+      // more residency than the scattered stores)
+      const size_t stage = (size_t)b->max_rows * 8;
+      sa.stage_off = 0;
+      if (sa.atom_ranks && b->max_rows <= kSortStageRows && smem + stage <= cap) {
+        sa.stage_off = (int)smem;
+        smem += stage;
       }
       auto kern = sw.seg ? (wide ? (nw == 16 ? sort_kernel<uint32_t, 16, true> : sort_kernel<uint32_t, 8, true>)
                                  : (nw == 16 ? sort_kernel<uint16_t, 16, true> : sort_kernel<uint16_t, 8, true>))
