@@ -365,17 +365,40 @@ __global__ void __launch_bounds__(128, FRIR_GEOM_MINB) geom_kernel(GeomArgs A) {
   for (int m = 0; m < M; ++m) {
     int2* out = items + (size_t)m * rows + wrow;
     const double mx = __ldg(mics + 3 * m), my = __ldg(mics + 3 * m + 1), mz = __ldg(mics + 3 * m + 2);
+    // delay_fast's arithmetic, branch-free for all 4 rows (rows past I are
+    // computed on valid data and never stored); the exact reference arithmetic
+    // runs only if some lane is within the 1e-14 guard band (warp-uniform test)
+    double d2[4], kc[4];
+    float inv_d[4];
+    bool guard = false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double dx = __dsub_rn(px[k], mx), dy = __dsub_rn(py[k], my), dz = __dsub_rn(pz[k], mz);
+      d2[k] = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+      const double y = rsqrt(d2[k]);  // CUDA: max 1 ulp
+      inv_d[k] = (float)y;
+      const double x = __dmul_rn(__dmul_rn(d2[k], y), rate_c0);
+      kc[k] = ceil(x);
+      const double eps = 1e-14 * x;
+      guard |= k < nk && (kc[k] - x < eps || x - (kc[k] - 1.0) < eps);
+    }
+    if (__any_sync(0xffffffffu, guard)) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double x = __dmul_rn(__dmul_rn(d2[k], rsqrt(d2[k])), rate_c0);
+        const double eps = 1e-14 * x;
+        if (k < nk && (kc[k] - x < eps || x - (kc[k] - 1.0) < eps))
+          kc[k] = ceil(__dmul_rn(__ddiv_rn(__dsqrt_rn(d2[k]), J.c0), A.rate));
+      }
+    }
     int2 it[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      it[k] = make_int2(0, 0);
-      if (k < nk) {
-        float inv_d;
-        const int q = delay_fast(px[k], py[k], pz[k], mx, my, mz, J.c0, A.rate, rate_c0, J.L + ism, &inv_d);
-        FRIR_CHECK(q >= 0 && q < J.L + ism && 4 * g + 1 + k < rows);
-        it[k] = q > J.L - 1 ? dropped_item(J.n2)  // ISM only: dropped arrival
-                            : make_item(q, lg[k] * inv_d, A.r_h, A.t0, A.rh_magic);  // r^g / D
-      }
+      const int Lx = J.L + ism;
+      const int q = kc[k] >= (double)(Lx - 1) ? Lx - 1 : (int)kc[k];
+      FRIR_CHECK(k >= nk || (q >= 0 && q < J.L + ism && 4 * g + 1 + k < rows));
+      it[k] = q > J.L - 1 ? dropped_item(J.n2)  // ISM only: dropped arrival
+                          : make_item(q, lg[k] * inv_d[k], A.r_h, A.t0, A.rh_magic);  // r^g / D
     }
     __syncwarp();
 #pragma unroll
