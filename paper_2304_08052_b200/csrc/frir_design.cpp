@@ -229,7 +229,7 @@ bool design(int fs, Design* out, std::string* err) {
   D.lpcoef = {d.c1, d.c2, std::real(v0[0]), std::imag(v0[0]), std::real(v0[1]), std::imag(v0[1])};
 
   double rho = std::abs(pole);
-  d.horizon = (int)std::ceil(std::log(1e-11) / std::log(rho));
+  d.horizon = (int)std::ceil(std::log(1e-9) / std::log(rho));  // items beyond feed < 1e-9 of their amplitude
   D.ppow.resize((size_t)2 * d.horizon);
   {
     cplx pm = 1.0;
