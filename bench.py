@@ -414,13 +414,19 @@ def run_ours(args):
     tot_render = float(sum(render_ms))
     tot_pre = float(sum(prerender_ms))
 
-    # ---- throughput (value): the K steps as a 2-deep pipeline.  Launches are
-    # independent batches, so launch k + 1's latency-bound geom/sort/tail
-    # kernels run on a second stream (own workspace and outputs) while launch k
-    # renders.  The per-launch working set (item lists + RIRs) exceeds L2.
-    outs = [(full, earlyb, direct),
-            (torch.empty_like(full), torch.empty_like(earlyb) if early else None, torch.empty_like(direct))]
-    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    # ---- throughput (value): launches are independent batches.  Small ones do
+    # not fill the GPU on their own, so they run as a 2-deep pipeline: launch
+    # k + 1's latency-bound geom/sort/tail kernels on a second stream (own
+    # workspace and outputs) while launch k renders.  Launches of >= 64 K
+    # channels (configs 3 and 5) fill it: there the render's three CTAs per SM
+    # leave no room for the other stream and one stream is measured faster
+    # (config 5: 309 vs 316 ms per step), so they run back to back.  The
+    # per-launch working set (item lists + RIRs) exceeds L2.
+    depth = 1 if min(int(db.batch.total_channels) for _, _, db in batches) >= 65536 else 2
+    outs = [(full, earlyb, direct)]
+    if depth == 2:
+        outs.append((torch.empty_like(full), torch.empty_like(earlyb) if early else None, torch.empty_like(direct)))
+    streams = [torch.cuda.Stream(dev) for _ in range(depth)]
 
     def pipelined(nsteps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -431,7 +437,7 @@ def run_ours(args):
         for _ in range(nsteps):
             for _, _, db in batches:
                 db.launch(*outs[slot], stream=streams[slot], workspace=wss[slot])
-                slot ^= 1
+                slot = (slot + 1) % depth
         for st_ in streams:
             ev_ = torch.cuda.Event()
             ev_.record(st_)
@@ -524,8 +530,10 @@ def run_ours(args):
                  "inst_per_launch": prof.get("inst_executed") if prof else None},
         "stages": {"serial_ms_per_step": max_serial / K, "serial_value": total_rirs * K / (max_serial / 1e3),
                    "render_ms_per_step": max_render / K, "pre_render_ms_per_step": max_pre / K,
+                   "value_streams": depth,
                    "note": "serial pass: one stream, geom+sort+tail then render per launch, 252 MB L2 flush "
-                           "between steps; value runs the same launches as a 2-stream pipeline"},
+                           "between steps; value runs the same launches back to back on value_streams streams "
+                           "(2: a pipeline for launches that do not fill the GPU)"},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "RIR/s", "h2d_bytes_per_step": e2e["h2d"] * world,
                 "d2h_bytes_per_step": e2e["d2h"] * world, "ms_per_step": e2e_ms,

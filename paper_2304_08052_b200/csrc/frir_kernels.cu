@@ -1545,7 +1545,9 @@ static cudaError_t launch_render(const frir_plan* plan, const RenderArgs& ra, lo
   const int per_sm = plan->lc.render_per_sm[EARLY][NBK - 1][SEG];
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   long want = (channels * ra.seg_max + kWarps - 1) / kWarps;  // upper bound of the work units
-  int grid = (int)std::min<long>((long)plan->lc.sms * per_sm, want);
+  static const int cap = getenv("FRIR_RENDER_CTAS") ? atoi(getenv("FRIR_RENDER_CTAS")) : 0;  // (experiment)
+  const int ctas = cap > 0 && cap < per_sm ? cap : per_sm;
+  int grid = (int)std::min<long>((long)plan->lc.sms * ctas, want);
   render_kernel<EARLY, NBK, SEG><<<grid, kRenderThreads, smem, st>>>(ra);
   return cudaGetLastError();
 }
