@@ -469,3 +469,18 @@ def test_sort_atomic_ranks_equal_ballot_ranks():
         assert res.returncode == 0, res.stderr[-2000:]
         outs.append(res.stdout)
     assert outs[0] == outs[1] and len(outs[0].splitlines()) == 4
+
+
+def test_shared_memory_limits_raise_clear_errors():
+    """Inputs the kernels cannot hold in shared memory fail at launch with a
+    clear FRIR_ERANGE message, not a generic CUDA error: a 60 s RIR (960,000
+    outputs: 30,000 sort buckets) and a 2 kHz plan (r_h = 500: render tables
+    past the shared-memory limit)."""
+    from paper_2304_08052_b200 import _abi
+
+    arr = F.linear_array([0.05])
+    scene = F.Scene(room_dims=(30.0, 25.0, 10.0), mic_positions=arr, sources=[(2.0, 0.3, 0.0)])
+    with pytest.raises(_abi.FrirLibraryError, match="too long for the per-channel sort"):
+        F.simulate_rir(F.SimParams(t60=60.0, num_images=64, seed=1), scene)
+    with pytest.raises(_abi.FrirLibraryError, match="shared memory|supported range"):
+        engine.Plan(2000, torch.cuda.current_device())
