@@ -484,3 +484,28 @@ def test_shared_memory_limits_raise_clear_errors():
         F.simulate_rir(F.SimParams(t60=60.0, num_images=0, seed=1), scene)  # (no images: no rr_max rule)
     with pytest.raises(_abi.FrirLibraryError, match="shared memory|supported range"):
         engine.Plan(2000, torch.cuda.current_device())
+
+
+def test_host_stream_equals_device_batch():
+    """engine.HostStream (bench.py's e2e path): parts of a job table rendered
+    through a ring of pinned host slots equal one DeviceBatch render."""
+    w = workloads.config5(6)
+    ref = engine.simulate_jobs(16000, w.jobs, w.mics, include_early=True)
+    hs = engine.HostStream(16000, w.jobs, w.mics, part_jobs=2, include_early=True, slots=2)
+    assert len(hs.parts) == 3 and hs.n_jobs == 6 and hs.d2h_bytes > 0 and hs.h2d_bytes > 0
+    seen = []
+
+    def check(k, host):
+        pb = hs.parts[k]
+        for jj in range(len(pb.jobs)):
+            J = pb.jobs[jj]
+            m, stride, n2, off = (int(J[f]) for f in ("n_mics", "out_stride", "n2", "out_off"))
+            for kind in ("full", "early"):
+                got = host[kind][off: off + m * stride].reshape(m, stride)[:, :n2]
+                assert np.array_equal(got, ref.job_view(2 * k + jj, kind).cpu().numpy())
+        seen.append(k)
+
+    for _ in range(2):  # the slots are reused across passes
+        seen.clear()
+        hs.run(consumer=check)
+        assert sorted(seen) == [0, 1, 2]
