@@ -135,14 +135,21 @@ __global__ void __launch_bounds__(32 * (1 + kEdcIo)) edc_kernel(const T* __restr
         for (int hh = 1; hh >= 0; --hh) {
           double sq[kEdcTile / 2];
 #pragma unroll
-          for (int k = 0; k < kEdcTile / 2; k += kVec) {  // 16-byte reads
-            T f[kVec];
-            *reinterpret_cast<float4*>(f) = *reinterpret_cast<const float4*>(&src[lane][hh * (kEdcTile / 2) + k]);
+          for (int k = 0; k < kEdcTile / 2; k += kVec) {  // 16-byte reads (registers, no local array)
+            if constexpr (sizeof(T) == 4) {
+              const float4 f4 = *reinterpret_cast<const float4*>(&src[lane][hh * (kEdcTile / 2) + k]);
+              const float f[4] = {f4.x, f4.y, f4.z, f4.w};
 #pragma unroll
-            for (int e = 0; e < kVec; ++e) {
-              const double v = (double)f[e];
-              sq[k + e] = v * v;  // numpy: h ** 2 in FP64 (exact for float32 samples)
-              mx = f[e] < 0 ? (-f[e] > mx ? -f[e] : mx) : (f[e] > mx ? f[e] : mx);
+              for (int e = 0; e < 4; ++e) {
+                const double v = (double)f[e];
+                sq[k + e] = v * v;  // numpy: h ** 2 in FP64 (exact for float32 samples)
+                mx = fmaxf(mx, fabsf(f[e]));
+              }
+            } else {
+              const double2 f2 = *reinterpret_cast<const double2*>(&src[lane][hh * (kEdcTile / 2) + k]);
+              sq[k] = f2.x * f2.x;
+              sq[k + 1] = f2.y * f2.y;
+              mx = fmax(mx, fmax(fabs(f2.x), fabs(f2.y)));
             }
           }
 #pragma unroll
