@@ -509,3 +509,10 @@ def test_host_stream_equals_device_batch():
         seen.clear()
         hs.run(consumer=check)
         assert sorted(seen) == [0, 1, 2]
+
+
+def test_empty_batch_is_a_no_op():
+    """An empty job table renders nothing and raises nothing (engine and C ABI)."""
+    jobs = engine.new_jobs(0)
+    res = engine.simulate_jobs(16000, jobs, np.zeros((0, 3)), include_early=True)
+    assert res.full.numel() == 0 and res.early.numel() == 0 and res.direct_index.numel() == 0
