@@ -4,6 +4,8 @@ device draws, against the oracle port of the reference (oracle/framrir_port.py,
 run on all host cores).  Config 4 adds two rooms whose sources draw the maximum
 image count (16,384 images = 16,385 rows > the 16,384-row segmentation
 threshold), so the segmented render and its seam kernel are covered at 48 kHz.
+Configs 2 and 5 also run in oracle mode: the reference's own host draws
+(ImageSet rows) are uploaded and the kernels render from them.
 
 Tolerance (north_star): max |y - y_ref| / max |y_ref| <= 1e-5 per (room,
 source, variant) over all channels; direct-path indices exact.  With
@@ -71,11 +73,23 @@ def _workload(cfg):
     return w
 
 
-@pytest.mark.parametrize("cfg", [2, 3, 4, 5])
-def test_config_sweep_matches_oracle(cfg):
+def _draws(kw):
+    """The reference's own ImageSet rows of one job (oracle: core.py:131-221)."""
+    d = P.draw(P.Job(**kw))
+    return d.distances, d.azimuths, d.elevations, d.reflections
+
+
+@pytest.mark.parametrize("cfg,mode", [(2, "native"), (3, "native"), (4, "native"), (5, "native"),
+                                      (2, "oracle"), (5, "oracle")])
+def test_config_sweep_matches_oracle(cfg, mode):
     w = _workload(cfg)
     t0 = time.perf_counter()
-    res = engine.simulate_jobs(w.sample_rate, w.jobs, w.mics, include_early=True)
+    draws = None
+    if mode == "oracle":  # the host draws uploaded as the kernels' input (oracle mode)
+        with ProcessPoolExecutor(max_workers=len(os.sched_getaffinity(0))) as ex:
+            rows = list(ex.map(_draws, [_job_kw(w, j) for j in range(len(w.jobs))], chunksize=4))
+        draws = tuple(np.concatenate([r[k] for r in rows]) for k in range(4))
+    res = engine.simulate_jobs(w.sample_rate, w.jobs, w.mics, include_early=True, draws=draws)
     full = res.full.cpu().numpy()
     early = res.early.cpu().numpy()
     direct = res.direct_index.cpu().numpy()
@@ -100,10 +114,12 @@ def test_config_sweep_matches_oracle(cfg):
         "max_rows": int(pj["n_images"].max()) + 1,
         "segmented_channels": int(sum(int(pj[j]["n_mics"]) for j in range(len(pj))
                                       if pj[j]["n_images"] + 1 > SEG_ROWS)),
-        "tolerance": TOL, "mode": "native device draws vs oracle/framrir_port.py (numpy+scipy)",
+        "tolerance": TOL,
+        "mode": ("native device draws" if mode == "native" else "oracle mode: the reference's host draws")
+        + " vs oracle/framrir_port.py (numpy+scipy)",
         "wall_s": time.perf_counter() - t0,
     }
-    _RECORD[f"cfg{cfg}"] = rec
+    _RECORD[f"cfg{cfg}" + ("" if mode == "native" else "_oracle_mode")] = rec
     out = os.environ.get("FRIR_PARITY_OUT")
     if out:
         with open(out, "w") as f:
