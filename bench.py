@@ -292,15 +292,15 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)", fp32
 
 
-def render_profile(cfg: int, chunk: int):
+def render_profile(cfg: int, rooms_per_launch: int):
     """The committed ncu capture of one render launch of this config and launch
-    size (profiles/render_ncu.json, written by tools/ncu_summary.py from an
-    `ncu --set full` run of this bench's command), or None."""
+    size (profiles/render_ncu.json, written by tools/render_profile_json.py
+    from an `ncu --set full` run of the same launch), or None."""
     p = ROOT / "profiles" / "render_ncu.json"
     if not p.exists():
         return None
     d = json.loads(p.read_text()).get(f"cfg{cfg}")
-    if not d or (cfg == 5 and d.get("rooms_per_launch") != chunk):
+    if not d or d.get("rooms_per_launch") != rooms_per_launch:
         return None
     return d
 
@@ -492,7 +492,7 @@ def run_ours(args):
     item_bytes = sum(int(db.batch.total_items) * 8 for _, _, db in batches)
     render_s_launch = max_render / K / launches / 1e3
     hbm_achieved = out_bytes / launches / render_s_launch / 1e9
-    prof = render_profile(cfg, chunk)
+    prof = render_profile(cfg, int(batches[0][0].rooms))
     chain_flops = sum(reference_chain_flops(pb.jobs, batches[0][0].sample_rate, variants) for _, pb, _ in batches)
     fp32_eff = chain_flops / (max_render / K / 1e3) / 1e12
     cpu = None
