@@ -116,11 +116,10 @@ def simulate_rir(params: SimParams, scene: Scene, include_early: bool = True, *,
     if not (0 <= int(params.seed) < 2**64):
         raise ValueError("seed must be in [0, 2**64)")
     jobs, mics = scene_jobs(params, scene)
-    res = engine.simulate_jobs(params.sample_rate, jobs, mics, include_early=include_early,
-                               device=device)
-    full_h = res.full.cpu().numpy()
-    early_h = res.early.cpu().numpy() if include_early else None
-    direct_h = res.direct_index.cpu().numpy().astype(np.int64)
+    # one launch sequence for all sources; one copy each way (engine.CallRunner)
+    pb, full_h, early_h, direct_h = engine.CallRunner.get(params.sample_rate, device).run(
+        jobs, mics, include_early=include_early)
+    direct_h = direct_h.astype(np.int64)
 
     meta_base = {
         "t60": params.t60, "seed": params.seed, "num_images": params.num_images,
@@ -132,7 +131,7 @@ def simulate_rir(params: SimParams, scene: Scene, include_early: bool = True, *,
     chain_meta = {"r_h": factors.r_h, "r_l": factors.r_l, "highpass_hz": HIGHPASS_HZ,
                   "direct_index_map": "round(high_rate_index / r_h)"}
     srcs = np.atleast_2d(np.asarray(scene.sources, dtype=float))
-    pj = res.prepared.jobs
+    pj = pb.jobs
     out = []
     for k in range(len(srcs)):
         meta = dict(meta_base, source_index=k, distance=float(srcs[k, 0]),

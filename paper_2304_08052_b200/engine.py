@@ -431,3 +431,87 @@ class HostStream:
             slot["done"], slot["part"] = done, k
         for slot in self.slots:
             self._retire(slot, consumer)
+
+
+class CallRunner:
+    """Low-latency path for one small batch per call (the drop-in
+    ``simulate_rir``, called per item by reference dataloaders,
+    mixture.py:342): the job tables travel in ONE pinned host→device copy, the
+    outputs (full, early, direct indices) come back in ONE device→host copy,
+    and the device tables, workspace and outputs are reused across calls
+    (grown on demand).  One runner per (sample rate, device); a lock keeps
+    concurrent callers from sharing its buffers."""
+
+    _runners: dict = {}
+    _runners_lock = threading.Lock()
+
+    @classmethod
+    def get(cls, sample_rate: int, device=None) -> "CallRunner":
+        require_cuda()
+        dev = torch.cuda.current_device() if device is None else torch.device(device).index
+        if dev is None:
+            dev = torch.cuda.current_device()
+        key = (int(sample_rate), dev)
+        with cls._runners_lock:
+            r = cls._runners.get(key)
+            if r is None:
+                r = cls._runners[key] = CallRunner(int(sample_rate), dev)
+        return r
+
+    def __init__(self, sample_rate: int, device: int):
+        self.sample_rate = sample_rate
+        self.dev = torch.device("cuda", device)
+        self.plan = get_plan(sample_rate, self.dev)
+        self.lock = threading.Lock()
+        self._bufs = {}
+
+    def _buf(self, name, nbytes, pinned=False):
+        b = self._bufs.get(name)
+        if b is None or b.numel() < nbytes:
+            n = max(int(nbytes), 1 << 16)
+            b = (torch.empty(n, dtype=torch.uint8).pin_memory() if pinned
+                 else torch.empty(n, dtype=torch.uint8, device=self.dev))
+            self._bufs[name] = b
+        return b
+
+    def run(self, jobs: np.ndarray, mics: np.ndarray, include_early: bool = True):
+        """(prepared batch, full, early or None, direct) with host numpy
+        arrays laid out as ``prepared.jobs`` says (copies, safe to keep)."""
+        pb = prepare(self.sample_rate, jobs, mics)
+        b = _abi.FrirBatch()
+        ctypes.memmove(ctypes.byref(b), ctypes.byref(pb.batch), ctypes.sizeof(b))
+        parts = [pb.jobs.view(np.uint8).reshape(-1), pb.chan_job.view(np.uint8), pb.chan_order.view(np.uint8),
+                 pb.mics.reshape(-1).view(np.uint8)]
+        offs, n = [], 0
+        for a in parts:
+            offs.append(n)
+            n = (n + a.nbytes + 255) & ~255
+        nout, nch = int(b.total_out), int(b.total_channels)
+        v = 2 if include_early else 1
+        out_bytes = nout * 4 * v + nch * 4
+        with self.lock, torch.cuda.device(self.dev):
+            st = torch.cuda.current_stream(self.dev)
+            h_in = self._buf("h_in", n, pinned=True)
+            d_in = self._buf("d_in", n)
+            hv = h_in.numpy()
+            for a, o in zip(parts, offs):
+                hv[o: o + a.nbytes] = a
+            d_in[:n].copy_(h_in[:n], non_blocking=True)
+            base = d_in.data_ptr()
+            b.jobs, b.chan_job, b.chan_order, b.mics = (base + o for o in offs)
+            need = int(_abi.lib().frir_workspace_size(self.plan.handle, ctypes.byref(b)))
+            ws = self._buf("ws", need)
+            d_out = self._buf("d_out", out_bytes)
+            h_out = self._buf("h_out", out_bytes, pinned=True)
+            o = d_out.data_ptr()
+            status = _abi.lib().frir_simulate(self.plan.handle, ctypes.byref(b), ws.data_ptr(), ws.numel(), o,
+                                              o + nout * 4 if include_early else None, o + nout * 4 * v,
+                                              st.cuda_stream)
+            _abi.check(status, "frir_simulate")
+            h_out[:out_bytes].copy_(d_out[:out_bytes], non_blocking=True)
+            st.synchronize()
+            raw = h_out.numpy()
+            full = raw[: nout * 4].view(np.float32).copy()
+            early = raw[nout * 4: nout * 8].view(np.float32).copy() if include_early else None
+            direct = raw[nout * 4 * v: out_bytes].view(np.int32).copy()
+        return pb, full, early, direct
