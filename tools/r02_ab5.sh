@@ -1,0 +1,6 @@
+T=${1:-ab}
+for c in "5 --rooms 1024" "2"; do
+  for L in paper_2304_08052_b200/lib/libfrir.so paper_2304_08052_b200/lib/libfrir_u2.so paper_2304_08052_b200/lib/libfrir_u8.so; do
+    FRIR_LIB=$L python tools/stage_time.py --cfg $c
+  done
+done 2>&1 | tee gpurun_out/${T}_stages.txt
