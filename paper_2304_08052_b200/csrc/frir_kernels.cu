@@ -169,26 +169,6 @@ __device__ __forceinline__ int delay_of(double px, double py, double pz, const d
   return k >= (double)(L - 1) ? L - 1 : (int)k;
 }
 
-// Hot-loop form of delay_of for the image rows: the distance comes from the
-// FP64 reciprocal square root (D = d2 * rsqrt(d2), ~2 ulp) instead of the
-// correctly rounded sqrt; x = D * rate / c0 then lies within ~1e-15 of the
-// reference's value, so outside the 1e-14 guard band the ceiling is
-// identical, and inside it the exact reference arithmetic runs (sqrt_rn,
-// div_rn).  Also returns 1/D (the gain's denominator) for free.
-__device__ __forceinline__ int delay_fast(double px, double py, double pz, double mx, double my, double mz,
-                                          double c0, double rate, double rate_c0, int L, float* inv_d) {
-  const double dx = __dsub_rn(px, mx), dy = __dsub_rn(py, my), dz = __dsub_rn(pz, mz);
-  const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-  const double y = rsqrt(d2);  // CUDA: max 1 ulp
-  const double d = __dmul_rn(d2, y);
-  *inv_d = (float)y;
-  const double x = __dmul_rn(d, rate_c0);
-  double k = ceil(x);
-  const double eps = 1e-14 * x;
-  if (k - x < eps || x - (k - 1.0) < eps) k = ceil(__dmul_rn(__ddiv_rn(__dsqrt_rn(d2), c0), rate));
-  return k >= (double)(L - 1) ? L - 1 : (int)k;
-}
-
 // Item of the (image, mic) pair: biased output-rate start s' + 64 (20 bits) and
 // the phase phi (10 bits) of the composite tables, gain in the second word.
 __device__ __forceinline__ int2 make_item(int q, float a, int r_h, int t0, unsigned magic) {
@@ -365,9 +345,14 @@ __global__ void __launch_bounds__(128, FRIR_GEOM_MINB) geom_kernel(GeomArgs A) {
   for (int m = 0; m < M; ++m) {
     int2* out = items + (size_t)m * rows + wrow;
     const double mx = __ldg(mics + 3 * m), my = __ldg(mics + 3 * m + 1), mz = __ldg(mics + 3 * m + 2);
-    // delay_fast's arithmetic, branch-free for all 4 rows (rows past I are
-    // computed on valid data and never stored); the exact reference arithmetic
-    // runs only if some lane is within the 1e-14 guard band (warp-uniform test)
+    // Hot-loop form of delay_of for the image rows: the distance comes from
+    // the FP64 reciprocal square root (D = d2 * rsqrt(d2), ~2 ulp) instead of
+    // the correctly rounded sqrt, so x = D * rate / c0 lies within ~1e-15 of
+    // the reference's value and outside the 1e-14 guard band the ceiling is
+    // identical; 1/D (the gain's denominator) comes for free.  Branch-free
+    // for all 4 rows (rows past I are computed on valid data and never
+    // stored); the exact reference arithmetic (sqrt_rn, div_rn) runs only if
+    // some lane is within the guard band (warp-uniform test).
     double d2[4], kc[4];
     float inv_d[4];
     bool guard = false;
