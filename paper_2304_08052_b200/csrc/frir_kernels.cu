@@ -169,6 +169,18 @@ __device__ __forceinline__ int delay_of(double px, double py, double pz, const d
   return k >= (double)(L - 1) ? L - 1 : (int)k;
 }
 
+// 1/sqrt(x) for normal x > 0 without the library's special-value branches:
+// the hardware approximation refined by two Newton steps (a few ulp; the
+// delay's guard band absorbs far more).
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double r = fma(-(x * y), y, 1.0);  // 1 - x y^2
+  y = fma(0.5 * y, r, y);
+  r = fma(-(x * y), y, 1.0);
+  return fma(0.5 * y, r, y);
+}
+
 // Item of the (image, mic) pair: biased output-rate start s' + 64 (20 bits) and
 // the phase phi (10 bits) of the composite tables, gain in the second word.
 __device__ __forceinline__ int2 make_item(int q, float a, int r_h, int t0, unsigned magic) {
@@ -360,7 +372,7 @@ __global__ void __launch_bounds__(128, FRIR_GEOM_MINB) geom_kernel(GeomArgs A) {
     for (int k = 0; k < 4; ++k) {
       const double dx = __dsub_rn(px[k], mx), dy = __dsub_rn(py[k], my), dz = __dsub_rn(pz[k], mz);
       d2[k] = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-      const double y = rsqrt(d2[k]);  // CUDA: max 1 ulp
+      const double y = rsqrt_nr(d2[k]);  // a few ulp, no branches
       inv_d[k] = (float)y;
       const double x = __dmul_rn(__dmul_rn(d2[k], y), rate_c0);
       kc[k] = ceil(x);
@@ -370,7 +382,7 @@ __global__ void __launch_bounds__(128, FRIR_GEOM_MINB) geom_kernel(GeomArgs A) {
     if (__any_sync(0xffffffffu, guard)) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const double x = __dmul_rn(__dmul_rn(d2[k], rsqrt(d2[k])), rate_c0);
+        const double x = __dmul_rn(__dmul_rn(d2[k], rsqrt_nr(d2[k])), rate_c0);
         const double eps = 1e-14 * x;
         if (k < nk && (kc[k] - x < eps || x - (kc[k] - 1.0) < eps))
           kc[k] = ceil(__dmul_rn(__ddiv_rn(__dsqrt_rn(d2[k]), J.c0), A.rate));
