@@ -458,6 +458,47 @@ struct SortArgs {
 // sorted buffer.  Only the counters live in smem, so long channels keep the
 // SM occupied.
 // Counter type CT: 16-bit (packed pairs) while rows <= 65535, else 32-bit.
+// One-shot TMA bulk copy global -> shared completing on an mbarrier (sm_90+
+// PTX; the row is staged without passing through registers).
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init_expect(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+
+// Counter of (bucket b, warp w): the lanes of one warp instruction hit
+// different buckets of the same warp, so consecutive buckets of a warp sit in
+// consecutive 32-bit words (distinct banks); the two 16-bit halves of a word
+// belong to warps 2k and 2k + 1, never to lanes of one instruction.
+template <typename CT>
+__device__ __forceinline__ int cnt_idx(int b, int w, int nbk) {
+  if constexpr (sizeof(CT) == 2)
+    return (((w >> 1) * nbk + b) << 1) | (w & 1);
+  else
+    return w * nbk + b;
+}
+
 template <typename CT>
 __device__ __forceinline__ void count_add(CT* cnt, int idx) {
   if constexpr (sizeof(CT) == 2)
@@ -466,8 +507,13 @@ __device__ __forceinline__ void count_add(CT* cnt, int idx) {
     atomicAdd(reinterpret_cast<unsigned*>(cnt) + idx, 1u);
 }
 
-template <typename CT, int NW, bool SEG>  // NW warps per channel (more for long rows); SEG: segment tables
-__global__ void __launch_bounds__(NW * 32) sort_kernel(SortArgs A) {
+// K > 0 (rows <= NW * 32 * K, atomic ranks, no segment tables): the channel's
+// raw row is read ONCE, by a TMA bulk copy into the shared-memory buffer at
+// stage_off; both passes read it there (pass 2 takes each thread's K items
+// into registers first), the scatter rewrites the buffer in sorted order and
+// the sorted row leaves in coalesced stores.
+template <typename CT, int NW, bool SEG, int K = 0>  // NW warps per channel (more for long rows); SEG: segment tables
+__global__ void __launch_bounds__(NW * 32, (K > 0 ? 1024 : 2048) / (NW * 32)) sort_kernel(SortArgs A) {
   constexpr int kSortWarps = NW, kSortThreads = NW * 32;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_wsum[kSortWarps];
@@ -480,51 +526,102 @@ __global__ void __launch_bounds__(NW * 32) sort_kernel(SortArgs A) {
   const size_t base = J.item_off + (size_t)m * rows;
   const int2* src = A.ws.items_raw + base;
   int2* dst = A.ws.items + base;
-  CT* s_cnt = reinterpret_cast<CT*>(smem);  // [nbk][warps]
+  CT* s_cnt = reinterpret_cast<CT*>(smem);  // (bucket, warp) counters at cnt_idx<CT>
   int2* s_sorted = A.stage_off ? reinterpret_cast<int2*>(smem + A.stage_off) : nullptr;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = nbk * kSortWarps;
   const int nwords = (int)((n * sizeof(CT) + 3) / 4);
+  // pass 1: per-warp histograms over a contiguous row chunk per warp (K > 0:
+  // whole 32-row groups per warp, the row held in registers)
+  const int chunk = K > 0 ? (rows + kSortThreads - 1) / kSortThreads * 32 : (rows + kSortWarps - 1) / kSortWarps;
+  const int r_lo = warp * chunk, r_hi = min(rows, r_lo + chunk);
+  // K > 0: the raw row lands in the staging buffer by one TMA bulk copy of
+  // its 16-byte-aligned cover (lead = 0 or 1 item before the row; the cover
+  // ends at most 8 bytes past it, inside the 256-byte-aligned workspace)
+  __shared__ __align__(8) unsigned long long s_bar;
+  const uintptr_t sa = reinterpret_cast<uintptr_t>(src);
+  const int lead = (int)((sa >> 3) & 1);
+  if constexpr (K > 0) {
+    if (tid == 0) {
+      const uintptr_t g0 = sa & ~(uintptr_t)15, g1 = (sa + 8 * (uintptr_t)rows + 15) & ~(uintptr_t)15;
+      const unsigned bar = smem_u32(&s_bar);
+      mbar_init_expect(bar, (unsigned)(g1 - g0));
+      bulk_g2s(smem_u32(s_sorted), reinterpret_cast<const void*>(g0), (unsigned)(g1 - g0), bar);
+    }
+  }
+  const int2* s_raw = K > 0 ? s_sorted + lead : nullptr;
   for (int i = tid; i < nwords; i += kSortThreads) reinterpret_cast<unsigned*>(s_cnt)[i] = 0u;
   __syncthreads();
-  // pass 1: per-warp histograms over a contiguous row chunk per warp
-  const int chunk = (rows + kSortWarps - 1) / kSortWarps;
-  const int r_lo = warp * chunk, r_hi = min(rows, r_lo + chunk);
+  if constexpr (K > 0) {
+    mbar_wait(smem_u32(&s_bar), 0);
+    for (int r = r_lo + lane; r < r_hi; r += 32)
+      count_add(s_cnt, cnt_idx<CT>((s_raw[r].x & 0xFFFFF) >> 5, warp, nbk));
+  } else {
 #pragma unroll 4
-  for (int r = r_lo + lane; r < r_hi; r += 32) {
-    const int b = (__ldg(&src[r].x) & 0xFFFFF) >> 5;
-    count_add(s_cnt, b * kSortWarps + warp);
+    for (int r = r_lo + lane; r < r_hi; r += 32) {
+      const int b = (__ldg(&src[r].x) & 0xFFFFF) >> 5;
+      count_add(s_cnt, cnt_idx<CT>(b, warp, nbk));
+    }
   }
   __syncthreads();
-  // exclusive scan over (bucket, warp) in bucket-major order: serial per
-  // thread, shuffles within a warp, one smem round across warps
-  const int per = (n + kSortThreads - 1) / kSortThreads;
-  const int lo = tid * per, hi = min(n, lo + per);
-  int sum = 0;
-  for (int i = lo; i < hi; ++i) sum += s_cnt[i];
-  int inc = sum;
+  // exclusive scan over (bucket, warp) in bucket-major order: thread t takes
+  // buckets t, t + T, ..., sums its bucket's NW counters in registers, the
+  // bucket totals are scanned across the CTA (shuffles, one smem round), and
+  // the NW positions are written back (one word per warp pair)
+  unsigned* s_w = reinterpret_cast<unsigned*>(s_cnt);
+  int carry = 0;
+  for (int b0 = 0; b0 < nbk; b0 += kSortThreads) {
+    const int b = b0 + tid;
+    constexpr int kWords = sizeof(CT) == 2 ? NW / 2 : NW;  // counter words of one bucket
+    int tot = 0;
+    if (b < nbk) {
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += v;
+      for (int k = 0; k < kWords; ++k) {
+        const unsigned wv = s_w[k * nbk + b];
+        tot += sizeof(CT) == 2 ? (int)((wv & 0xFFFFu) + (wv >> 16)) : (int)wv;
+      }
+    }
+    int inc = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
+    }
+    if (lane == 31) s_wsum[warp] = inc;
+    __syncthreads();
+    const int ws = lane < kSortWarps ? s_wsum[lane] : 0;  // warp totals scanned by lanes
+    int wi = ws;
+#pragma unroll
+    for (int o = 1; o < kSortWarps; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += v;
+    }
+    int run = carry + inc - tot + __shfl_sync(0xffffffffu, wi - ws, warp);
+    const int all = __shfl_sync(0xffffffffu, wi, kSortWarps - 1);
+    if (b < nbk) {
+#pragma unroll
+      for (int k = 0; k < kWords; ++k) {  // (the words are read again: fewer live registers)
+        const unsigned wv = s_w[k * nbk + b];
+        if constexpr (sizeof(CT) == 2) {
+          const unsigned lo16 = wv & 0xFFFFu;
+          s_w[k * nbk + b] = (unsigned)run | ((unsigned)(run + lo16) << 16);
+          run += (int)(lo16 + (wv >> 16));
+        } else {
+          s_w[k * nbk + b] = (unsigned)run;
+          run += (int)wv;
+        }
+      }
+    }
+    carry += all;
+    __syncthreads();
   }
-  if (lane == 31) s_wsum[warp] = inc;
-  __syncthreads();
-  int run = inc - sum;
-  for (int w2 = 0; w2 < warp; ++w2) run += s_wsum[w2];
-  for (int i = lo; i < hi; ++i) {
-    const int cnt = s_cnt[i];
-    s_cnt[i] = (CT)run;
-    run += cnt;
-  }
-  __syncthreads();
-  const int nvalid = (int)s_cnt[(nbk - 1) * kSortWarps];  // items before the dropped-arrival bucket
+  const int nvalid = (int)s_cnt[cnt_idx<CT>(nbk - 1, 0, nbk)];  // items before the dropped-arrival bucket
   if (tid == 0) A.ws.chan_rows[c] = nvalid;
   const int S = SEG ? seg_count(nvalid, J.n2) : 1;
   if (SEG && tid == 0) A.sw.seg[(size_t)c * kSegInts + 63] = S;  // read by K3 / K4
   if (S > 1) {
     // segment boundaries of a long channel: whole tiles, about rows / S items
-    // each, every segment at least one tile.  s_cnt[b * NW] is now the number
+    // each, every segment at least one tile.  s_cnt at (b, 0) is now the number
     // of items in buckets < b.  Bucket b feeds windows b - 2 .. b - 2 + tbk
     // (tbk = 32-tap table blocks), so segment k renders windows [W_k, W_k+1)
     // from the items of buckets [W_k + 2 - tbk, W_k+1 + 1].
@@ -532,7 +629,7 @@ __global__ void __launch_bounds__(NW * 32) sort_kernel(SortArgs A) {
       const int nwin = (J.n2 + kExt + kWin - 1) / kWin;
       const int top = (nwin / kTileWin) * kTileWin;  // last segment start <= top - kTileWin
       const int tbk = (A.plan.d.sup + 31) / 32;
-      auto start = [&](int b) { return (int)s_cnt[b * kSortWarps]; };
+      auto start = [&](int b) { return (int)s_cnt[cnt_idx<CT>(b, 0, nbk)]; };
       int* seg = A.sw.seg + (size_t)c * kSegInts;
       int wprev = 0;
       seg[0] = 0;
@@ -562,6 +659,33 @@ __global__ void __launch_bounds__(NW * 32) sort_kernel(SortArgs A) {
   // pass 2: stable scatter, warp w walks its chunk in row order; early flags
   // (core.py:259-264) from the channel's direct arrival q0
   const int q0 = A.ws.chan_q0[c];
+  if constexpr (K > 0) {
+    int2 reg[K];  // the warp's rows leave the buffer before the scatter rewrites it
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int r = r_lo + 32 * k + lane;
+      reg[k] = r < r_hi ? s_raw[r] : make_int2(0, 0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (r_lo + 32 * k + lane < r_hi) {
+        int2 it = reg[k];
+        const int sp = (it.x & 0xFFFFF) - kSpBias - kExt;
+        const int phi = ((unsigned)it.x >> 20) & 0x3FF;
+        const int rel = A.r_h * sp - A.t0 - phi - q0;  // q - q0
+        if (rel >= -J.e_lo && rel <= J.e_hi) it.y ^= 0x80000000;  // early: negative gain
+        const int idx = cnt_idx<CT>((it.x & 0xFFFFF) >> 5, warp, nbk);
+        const unsigned sh = 16u * (idx & 1);
+        const int pos = (int)((atomicAdd(reinterpret_cast<unsigned*>(s_cnt) + (idx >> 1), 1u << sh) >> sh) & 0xFFFFu);
+        FRIR_CHECK(pos >= 0 && pos < rows);
+        s_sorted[pos] = it;
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < rows; i += kSortThreads) dst[i] = s_sorted[i];
+    return;
+  }
   int2 v = r_lo + lane < r_hi ? src[r_lo + lane] : make_int2(0, 0);
   if (A.atom_ranks) {
     // ranks from the shared-memory atomics: each item takes its bucket's
@@ -578,7 +702,7 @@ __global__ void __launch_bounds__(NW * 32) sort_kernel(SortArgs A) {
         const int phi = ((unsigned)it.x >> 20) & 0x3FF;
         const int rel = A.r_h * sp - A.t0 - phi - q0;  // q - q0
         if (rel >= -J.e_lo && rel <= J.e_hi) it.y ^= 0x80000000;  // early: negative gain
-        const int idx = ((it.x & 0xFFFFF) >> 5) * kSortWarps + warp;
+        const int idx = cnt_idx<CT>((it.x & 0xFFFFF) >> 5, warp, nbk);
         int pos;
         if constexpr (sizeof(CT) == 2) {
           const unsigned sh = 16u * (idx & 1);
@@ -611,7 +735,7 @@ __global__ void __launch_bounds__(NW * 32) sort_kernel(SortArgs A) {
     const int b = ok ? (it.x & 0xFFFFF) >> 5 : nbk + lane;  // distinct for idle lanes
     const unsigned peers = peers_of(b, kbits);  // lanes with the same bucket
     const int rank = __popc(peers & ((1u << lane) - 1u));
-    CT* slot = s_cnt + (ok ? b * kSortWarps + warp : 0);
+    CT* slot = s_cnt + (ok ? cnt_idx<CT>(b, warp, nbk) : 0);
     const int pos = ok ? *slot + rank : 0;
     FRIR_CHECK(!ok || (pos >= 0 && pos < rows && b < nbk));
     __syncwarp();
@@ -1523,6 +1647,10 @@ cudaError_t init_launch_cache(frir_plan* p) {
   if (e == cudaSuccess) e = allow_smem(sort_kernel<uint16_t, 16, true>, mx);
   if (e == cudaSuccess) e = allow_smem(sort_kernel<uint32_t, 8, true>, mx);
   if (e == cudaSuccess) e = allow_smem(sort_kernel<uint32_t, 16, true>, mx);
+  if (e == cudaSuccess) e = allow_smem(sort_kernel<uint16_t, 8, false, 8>, mx);
+  if (e == cudaSuccess) e = allow_smem(sort_kernel<uint16_t, 8, false, 16>, mx);
+  if (e == cudaSuccess) e = allow_smem(sort_kernel<uint16_t, 16, false, 8>, mx);
+  if (e == cudaSuccess) e = allow_smem(sort_kernel<uint16_t, 16, false, 16>, mx);
   if (e == cudaSuccess) e = allow_smem(tail_kernel<false>, mx);
   if (e == cudaSuccess) e = allow_smem(tail_kernel<true>, mx);
   if (e == cudaSuccess) e = init_render<true, 1, false>(p);
@@ -1619,13 +1747,18 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_
       // short rows: the scatter goes to shared memory first (<= 36 KB) and the
       // sorted row leaves in coalesced stores (longer rows: the buffer costs
       // more residency than the scattered stores)
-      const size_t stage = (size_t)b->max_rows * 8;
+      const size_t stage = (size_t)b->max_rows * 8 + 16;  // (+16: the K > 0 path's aligned TMA cover)
       sa.stage_off = 0;
-      if (sa.atom_ranks && b->max_rows <= kSortStageRows && smem + stage <= cap) {
+      // rows that fit nw * 32 * K registers: read once into registers (K > 0)
+      const int kreg = (!sa.atom_ranks || wide || sw.seg || smem + stage > cap) ? 0
+                       : b->max_rows <= nw * 32 * 8 ? 8 : b->max_rows <= nw * 32 * 16 ? 16 : 0;
+      if (kreg || (sa.atom_ranks && b->max_rows <= kSortStageRows && smem + stage <= cap)) {
         sa.stage_off = (int)smem;
         smem += stage;
       }
-      auto kern = sw.seg ? (wide ? (nw == 16 ? sort_kernel<uint32_t, 16, true> : sort_kernel<uint32_t, 8, true>)
+      auto kern = kreg ? (nw == 16 ? (kreg == 8 ? sort_kernel<uint16_t, 16, false, 8> : sort_kernel<uint16_t, 16, false, 16>)
+                                   : (kreg == 8 ? sort_kernel<uint16_t, 8, false, 8> : sort_kernel<uint16_t, 8, false, 16>))
+                 : sw.seg ? (wide ? (nw == 16 ? sort_kernel<uint32_t, 16, true> : sort_kernel<uint32_t, 8, true>)
                                  : (nw == 16 ? sort_kernel<uint16_t, 16, true> : sort_kernel<uint16_t, 8, true>))
                          : (wide ? (nw == 16 ? sort_kernel<uint32_t, 16, false> : sort_kernel<uint32_t, 8, false>)
                                  : (nw == 16 ? sort_kernel<uint16_t, 16, false> : sort_kernel<uint16_t, 8, false>));
