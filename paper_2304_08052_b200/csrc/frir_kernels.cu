@@ -1648,9 +1648,9 @@ cudaError_t init_launch_cache(frir_plan* p) {
   if (e == cudaSuccess) e = allow_smem(sort_kernel<uint32_t, 8, true>, mx);
   if (e == cudaSuccess) e = allow_smem(sort_kernel<uint32_t, 16, true>, mx);
   if (e == cudaSuccess) e = allow_smem(sort_kernel<uint16_t, 8, false, 8>, mx);
-  if (e == cudaSuccess) e = allow_smem(sort_kernel<uint16_t, 8, false, 16>, mx);
+  if (e == cudaSuccess) e = allow_smem(sort_kernel<uint16_t, 8, false, 17>, mx);
   if (e == cudaSuccess) e = allow_smem(sort_kernel<uint16_t, 16, false, 8>, mx);
-  if (e == cudaSuccess) e = allow_smem(sort_kernel<uint16_t, 16, false, 16>, mx);
+  if (e == cudaSuccess) e = allow_smem(sort_kernel<uint16_t, 16, false, 17>, mx);
   if (e == cudaSuccess) e = allow_smem(tail_kernel<false>, mx);
   if (e == cudaSuccess) e = allow_smem(tail_kernel<true>, mx);
   if (e == cudaSuccess) e = init_render<true, 1, false>(p);
@@ -1749,15 +1749,16 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_
       // more residency than the scattered stores)
       const size_t stage = (size_t)b->max_rows * 8 + 16;  // (+16: the K > 0 path's aligned TMA cover)
       sa.stage_off = 0;
-      // rows that fit nw * 32 * K registers: read once into registers (K > 0)
+      // rows that fit nw * 32 * K registers: read once into registers (K > 0; K = 17
+      // covers config 5's longest rows, I = 8192 -> 8193 rows, with 16 warps)
       const int kreg = (!sa.atom_ranks || wide || sw.seg || smem + stage > cap) ? 0
-                       : b->max_rows <= nw * 32 * 8 ? 8 : b->max_rows <= nw * 32 * 16 ? 16 : 0;
+                       : b->max_rows <= nw * 32 * 8 ? 8 : b->max_rows <= nw * 32 * 17 ? 17 : 0;
       if (kreg || (sa.atom_ranks && b->max_rows <= kSortStageRows && smem + stage <= cap)) {
         sa.stage_off = (int)smem;
         smem += stage;
       }
-      auto kern = kreg ? (nw == 16 ? (kreg == 8 ? sort_kernel<uint16_t, 16, false, 8> : sort_kernel<uint16_t, 16, false, 16>)
-                                   : (kreg == 8 ? sort_kernel<uint16_t, 8, false, 8> : sort_kernel<uint16_t, 8, false, 16>))
+      auto kern = kreg ? (nw == 16 ? (kreg == 8 ? sort_kernel<uint16_t, 16, false, 8> : sort_kernel<uint16_t, 16, false, 17>)
+                                   : (kreg == 8 ? sort_kernel<uint16_t, 8, false, 8> : sort_kernel<uint16_t, 8, false, 17>))
                  : sw.seg ? (wide ? (nw == 16 ? sort_kernel<uint32_t, 16, true> : sort_kernel<uint32_t, 8, true>)
                                  : (nw == 16 ? sort_kernel<uint16_t, 16, true> : sort_kernel<uint16_t, 8, true>))
                          : (wide ? (nw == 16 ? sort_kernel<uint32_t, 16, false> : sort_kernel<uint32_t, 8, false>)
