@@ -679,11 +679,26 @@ __global__ void __launch_bounds__(NW * 32, (K > 0 ? 1024 : 2048) / (NW * 32)) so
         const unsigned sh = 16u * (idx & 1);
         const int pos = (int)((atomicAdd(reinterpret_cast<unsigned*>(s_cnt) + (idx >> 1), 1u << sh) >> sh) & 0xFFFFu);
         FRIR_CHECK(pos >= 0 && pos < rows);
-        s_sorted[pos] = it;
+        s_sorted[lead + pos] = it;  // the sorted row keeps dst's alignment mod 16
       }
     }
+    // the sorted row leaves by one TMA bulk store of its 16-byte-aligned
+    // interior (the async proxy reads smem written by st.shared: fence first);
+    // the <= 1 item before and after it go by plain stores
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    for (int i = tid; i < rows; i += kSortThreads) dst[i] = s_sorted[i];
+    if (tid == 0) {
+      const int i0 = lead, n_int = (rows - i0) & ~1;  // dst + i0 is 16-byte aligned (same offset as src)
+      if (lead) dst[0] = s_sorted[1];
+      if (i0 + n_int < rows) dst[rows - 1] = s_sorted[lead + rows - 1];
+      if (n_int > 0) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + i0),
+                     "r"(smem_u32(s_sorted + lead + i0)), "r"((unsigned)n_int * 8u)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem read before the CTA exits
+      }
+    }
     return;
   }
   int2 v = r_lo + lane < r_hi ? src[r_lo + lane] : make_int2(0, 0);
