@@ -169,15 +169,12 @@ __device__ __forceinline__ int delay_of(double px, double py, double pz, const d
   return k >= (double)(L - 1) ? L - 1 : (int)k;
 }
 
-// 1/sqrt(x) for normal x > 0 without the library's special-value branches:
-// the hardware approximation refined by two Newton steps (a few ulp; the
-// delay's guard band absorbs far more).
-__device__ __forceinline__ double rsqrt_nr(double x) {
+// 1/sqrt(x) for normal x > 0: the hardware approximation (relative error
+// <= 2^-20) refined by one Newton step (<= 1.4e-12).
+__device__ __forceinline__ double rsqrt_nr1(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double r = fma(-(x * y), y, 1.0);  // 1 - x y^2
-  y = fma(0.5 * y, r, y);
-  r = fma(-(x * y), y, 1.0);
+  const double r = fma(-(x * y), y, 1.0);  // 1 - x y^2
   return fma(0.5 * y, r, y);
 }
 
@@ -358,35 +355,34 @@ __global__ void __launch_bounds__(128, FRIR_GEOM_MINB) geom_kernel(GeomArgs A) {
     int2* out = items + (size_t)m * rows + wrow;
     const double mx = __ldg(mics + 3 * m), my = __ldg(mics + 3 * m + 1), mz = __ldg(mics + 3 * m + 2);
     // Hot-loop form of delay_of for the image rows: the distance comes from
-    // the FP64 reciprocal square root (D = d2 * rsqrt(d2), ~2 ulp) instead of
-    // the correctly rounded sqrt, so x = D * rate / c0 lies within ~1e-15 of
-    // the reference's value and outside the 1e-14 guard band the ceiling is
-    // identical; 1/D (the gain's denominator) comes for free.  Branch-free
-    // for all 4 rows (rows past I are computed on valid data and never
-    // stored); the exact reference arithmetic (sqrt_rn, div_rn) runs only if
-    // some lane is within the guard band (warp-uniform test).
+    // the FP64 reciprocal square root with ONE Newton step (D = d2 * rsqrt(d2);
+    // relative error <= 1.4e-12: 1.5 e0^2 for the hardware approximation's
+    // e0 <= 2^-20, measured by tools/checks/rsqrt_err.cu) instead of the
+    // correctly rounded sqrt, so x = D * rate / c0 lies within ~1.5e-12 x of
+    // the reference's value; outside a 2e-12 L guard band around the integers
+    // the ceiling is identical (x >= L clamps to L - 1 either way), and 1/D (the
+    // gain's denominator) comes for free.  Branch-free for all 4 rows (rows
+    // past I are computed on valid data and never stored); the exact reference
+    // arithmetic (sqrt_rn, div_rn) runs only for rows in the band (~1e-6 of
+    // them; warp-uniform test).
     double d2[4], kc[4];
     float inv_d[4];
-    bool guard = false;
+    const double half_band = 0.5 - 2e-12 * (double)(J.L + ism);
+    unsigned gm = 0;  // rows in the guard band
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const double dx = __dsub_rn(px[k], mx), dy = __dsub_rn(py[k], my), dz = __dsub_rn(pz[k], mz);
       d2[k] = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-      const double y = rsqrt_nr(d2[k]);  // a few ulp, no branches
+      const double y = rsqrt_nr1(d2[k]);  // no branches
       inv_d[k] = (float)y;
       const double x = __dmul_rn(__dmul_rn(d2[k], y), rate_c0);
       kc[k] = ceil(x);
-      const double eps = 1e-14 * x;
-      guard |= k < nk && (kc[k] - x < eps || x - (kc[k] - 1.0) < eps);
+      if (k < nk && fabs(__dsub_rn(kc[k], x) - 0.5) > half_band) gm |= 1u << k;  // |frac - 1/2| > 1/2 - band
     }
-    if (__any_sync(0xffffffffu, guard)) {
+    if (__any_sync(0xffffffffu, gm != 0u)) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const double x = __dmul_rn(__dmul_rn(d2[k], rsqrt_nr(d2[k])), rate_c0);
-        const double eps = 1e-14 * x;
-        if (k < nk && (kc[k] - x < eps || x - (kc[k] - 1.0) < eps))
-          kc[k] = ceil(__dmul_rn(__ddiv_rn(__dsqrt_rn(d2[k]), J.c0), A.rate));
-      }
+      for (int k = 0; k < 4; ++k)
+        if ((gm >> k) & 1u) kc[k] = ceil(__dmul_rn(__ddiv_rn(__dsqrt_rn(d2[k]), J.c0), A.rate));
     }
     int2 it[4];
 #pragma unroll
@@ -1343,9 +1339,13 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(const __grid_
           e_dead = fabs(sE0) + fabs(sE1) < fmax(1e-50, 0x1p-44 * e_ref);
         } else {
           const int n0 = n_base + kChunk * lane;
+          if (n0 >= 0 && n0 + kChunk <= nrow) {  // (rows are 16-byte aligned, n_base % 4 == 0)
+            *reinterpret_cast<float4*>(outE + n0) = make_float4(0.f, 0.f, 0.f, 0.f);
+          } else {
 #pragma unroll
-          for (int k = 0; k < kChunk; ++k)
-            if (n0 + k >= 0 && n0 + k < nrow) outE[n0 + k] = 0.f;
+            for (int k = 0; k < kChunk; ++k)
+              if (n0 + k >= 0 && n0 + k < nrow) outE[n0 + k] = 0.f;
+          }
         }
       }
       if (SEG && w == nwin - 1 && lane == 0) {  // last tile of the sweep: zero-start end state of a segment (K4)
