@@ -43,6 +43,7 @@ struct Workspace {
   int2* items_raw;  // per channel, image order (K1 -> K2)
   int* chan_q0;
   int* chan_rows;   // items per channel before the dropped-arrival bucket (K2 -> K2b, K3)
+  int* chan_tail;   // first item of the HP-horizon suffix per channel (K2 -> K2b)
   float* chan_scale;
   double* corr;     // per channel [F, E][32]: tail corrections of outputs n_c + i (K2 -> K3)
   int* counter;
@@ -89,6 +90,7 @@ Workspace carve(void* base, const frir_batch* b) {
   w.items_raw = (int2*)p; p += raw_bytes(b);
   w.chan_q0 = (int*)p; p += align_up((size_t)b->total_channels * 4);
   w.chan_rows = (int*)p; p += align_up((size_t)b->total_channels * 4);
+  w.chan_tail = (int*)p; p += align_up((size_t)b->total_channels * 4);
   w.chan_scale = (float*)p; p += align_up((size_t)b->total_channels * 4);
   w.corr = (double*)p; p += align_up((size_t)b->total_channels * 64 * 8);
   w.counter = (int*)p;
@@ -100,7 +102,7 @@ SegWs carve_seg(void* base, const frir_batch* b) {
   SegWs g{nullptr, nullptr, nullptr, nullptr};
   if (batch_seg_max(b) <= 1) return g;
   char* p = (char*)base + align_up((size_t)b->total_items * 8) + raw_bytes(b) +
-            3 * align_up((size_t)b->total_channels * 4) + align_up((size_t)b->total_channels * 64 * 8) + 256;
+            4 * align_up((size_t)b->total_channels * 4) + align_up((size_t)b->total_channels * 64 * 8) + 256;
   g.seg = (int*)p; p += align_up((size_t)b->total_channels * kSegInts * 4);
   g.state = (double*)p; p += align_up((size_t)b->total_channels * kMaxSeg * 4 * 8);
   g.units = (int*)p; p += align_up((size_t)b->total_channels * kMaxSeg * 4);
@@ -469,6 +471,13 @@ __device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned
                "l"(src), "r"(bytes), "r"(bar)
                : "memory");
 }
+__device__ __forceinline__ void mbar_init(unsigned bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned phase) {
   asm volatile(
       "{\n"
@@ -612,7 +621,26 @@ __global__ void __launch_bounds__(NW * 32, (K > 0 ? 1024 : 2048) / (NW * 32)) so
     __syncthreads();
   }
   const int nvalid = (int)s_cnt[cnt_idx<CT>(nbk - 1, 0, nbk)];  // items before the dropped-arrival bucket
-  if (tid == 0) A.ws.chan_rows[c] = nvalid;
+  if (tid == 0) {
+    A.ws.chan_rows[c] = nvalid;
+    // K2b's HP-horizon suffix starts at the first bucket whose items can feed
+    // the state at n1 (k_hi >= n1 - horizon; bucket b bounds q by qmax(b)).
+    // Counter (b, warp 0) is bucket b's start; only warp 0 advances it.
+    const frir_plan_desc& d = A.plan.d;
+    const long long kthr = (long long)J.n1 - d.horizon;
+    int p_t = 0;
+    if (kthr > 0) {
+      int lo = 0, hi = nbk - 1;  // smallest b not below the horizon (nbk - 1: none)
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const long long qmax = (long long)d.r_h * ((mid << 5) + 31 - kSpBias - kExt) - d.t0;
+        if ((long long)d.up * qmax + d.half1 < kthr * d.down) lo = mid + 1; else hi = mid;
+      }
+      p_t = min((int)s_cnt[cnt_idx<CT>(lo, 0, nbk)], nvalid);
+    }
+    A.ws.chan_tail[c] = p_t;
+  }
+  __syncwarp();  // lane 0 read warp 0's counters before the scatter advances them
   const int S = SEG ? seg_count(nvalid, J.n2) : 1;
   if (SEG && tid == 0) A.sw.seg[(size_t)c * kSegInts + 63] = S;  // read by K3 / K4
   if (S > 1) {
@@ -779,6 +807,7 @@ struct TailArgs {
 
 constexpr int kTailThreads = 128;
 constexpr int kTailWarps = kTailThreads / 32;
+constexpr int kTailChunk = 256;  // items per TMA chunk of the suffix (2 chunks in flight per warp)
 
 template <bool SPLIT>
 __global__ void __launch_bounds__(kTailThreads) tail_kernel(const __grid_constant__ TailArgs A) {
@@ -790,7 +819,9 @@ __global__ void __launch_bounds__(kTailThreads) tail_kernel(const __grid_constan
   double2* s_plo = reinterpret_cast<double2*>(smem);  // p^i, i < 128
   double2* s_zph = s_plo + 128;                      // Z[rho], rho < down
   double2* s_phi = s_zph + d.down;                   // p^(128 j)
-  double* s_xt = reinterpret_cast<double*>(s_phi + nphi);  // [warp][F, E][ltc]
+  double* s_xt = reinterpret_cast<double*>(s_phi + nphi);  // [warp][F, E][ltc], then the chunk buffers
+  __shared__ __align__(8) unsigned long long s_bar[kTailWarps][2];
+  if ((threadIdx.x & 31) < 2) mbar_init(smem_u32(&s_bar[threadIdx.x >> 5][threadIdx.x & 1]));
   for (int i = threadIdx.x; i < 128; i += blockDim.x) s_plo[i] = make_double2(P.ppow_lo[2 * i], P.ppow_lo[2 * i + 1]);
   for (int i = threadIdx.x; i < d.down; i += blockDim.x) s_zph[i] = make_double2(P.zphase[2 * i], P.zphase[2 * i + 1]);
   for (int i = threadIdx.x; i < nphi; i += blockDim.x) s_phi[i] = make_double2(P.ppow_hi[2 * i], P.ppow_hi[2 * i + 1]);
@@ -813,25 +844,7 @@ __global__ void __launch_bounds__(kTailThreads) tail_kernel(const __grid_constan
   for (int i = lane; i < 2 * ltc; i += 32) xt_s[i] = 0.0;
   __syncwarp();
 
-  // suffix start: earlier items have bucket <= a batch's first bucket, which
-  // bounds their k_hi
-  int p_t = 0;
-  if (kthr > 0) {
-    const int nb = (rows + 31) >> 5;
-    p_t = -1;
-    for (int b0 = nb - 1; b0 >= 0 && p_t < 0; b0 -= 32) {  // 32 batch starts per round
-      const int b = b0 - lane;
-      bool below = true;  // every item before batch b has k_hi < kthr
-      if (b > 0) {
-        const int bkf = (items[32 * b].x & 0xFFFFF) >> 5;
-        const long long qmax = (long long)r_h * ((bkf << 5) + 31 - kSpBias - kExt) - d.t0;
-        below = (long long)up * qmax + half1 < (long long)kthr * down;
-      }
-      const unsigned bm = __ballot_sync(0xffffffffu, b >= 0 && below);
-      if (bm) p_t = 32 * (b0 - (__ffs(bm) - 1));
-    }
-    p_t = max(p_t, 0);
-  }
+  int p_t = A.ws.chan_tail[c];  // HP-horizon suffix start (K2)
   int p_hi = rows;  // this warp's part of the suffix [p_t, p_hi)
   if (SPLIT) {
     const int chunk = ((rows - p_t + 32 * kTailWarps - 1) / (32 * kTailWarps)) * 32;
@@ -876,20 +889,35 @@ __global__ void __launch_bounds__(kTailThreads) tail_kernel(const __grid_constan
   // per batch a shuffle tree, batches in row order) and they are processed once.
   const int q_last = J.L - 1;
   double clampF = 0.0, clampE = 0.0;
-  constexpr int kGroup = 8;  // batches loaded together (memory-level parallelism)
-  for (int p0 = p_t; p0 < p_hi; p0 += 32 * kGroup) {
-  int2 grp[kGroup];
-#pragma unroll
-  for (int u = 0; u < kGroup; ++u) {
-    const int idx = p0 + 32 * u + lane;
-    grp[u] = idx < p_hi ? items[idx] : make_int2(0xFFFFF, 0);
-  }
-#pragma unroll
-  for (int u = 0; u < kGroup; ++u) {
-    const int p = p0 + 32 * u;
-    if (p >= p_hi) break;
-    const int2 it = grp[u];
-    const int cnt = min(32, p_hi - p);
+  // The suffix streams through a per-warp double buffer in shared memory:
+  // lane 0 issues TMA bulk copies of kTailChunk items (their 16-byte-aligned
+  // cover) one chunk ahead, so the loads are in flight while the warp works
+  // through the current chunk's batches.
+  int2* stage = reinterpret_cast<int2*>(s_xt + 2 * ltc * kTailWarps) + warp * 2 * (kTailChunk + 2);
+  const unsigned bar0 = smem_u32(&s_bar[warp][0]);
+  const int nchunk = p_hi > p_t ? (p_hi - p_t + kTailChunk - 1) / kTailChunk : 0;
+  auto issue = [&](int ci) {  // (lane 0)
+    const int lo = p_t + ci * kTailChunk, hi = min(p_hi, lo + kTailChunk);
+    const uintptr_t g0 = reinterpret_cast<uintptr_t>(items + lo) & ~(uintptr_t)15;
+    const uintptr_t g1 = (reinterpret_cast<uintptr_t>(items + hi) + 15) & ~(uintptr_t)15;
+    const unsigned bar = bar0 + 8u * (ci & 1);
+    mbar_arrive_expect(bar, (unsigned)(g1 - g0));
+    bulk_g2s(smem_u32(stage + (ci & 1) * (kTailChunk + 2)), reinterpret_cast<const void*>(g0), (unsigned)(g1 - g0), bar);
+  };
+  if (lane == 0 && nchunk > 0) issue(0);
+  for (int ci = 0; ci < nchunk; ++ci) {
+    __syncwarp();  // every lane is done with chunk ci - 1 (its buffer is refilled next)
+    if (lane == 0 && ci + 1 < nchunk) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(ci + 1);
+    }
+    mbar_wait(bar0 + 8u * (ci & 1), (ci >> 1) & 1);
+    const int c_lo = p_t + ci * kTailChunk, c_hi = min(p_hi, c_lo + kTailChunk);
+    const int2* buf = stage + (ci & 1) * (kTailChunk + 2) + (int)((reinterpret_cast<uintptr_t>(items + c_lo) >> 3) & 1);
+  for (int p = c_lo; p < c_hi; p += 32) {
+    const int cnt = min(32, c_hi - p);
+    const int2 it = lane < cnt ? buf[p - c_lo + lane] : make_int2(0xFFFFF, 0);
+    {
     const int spb = it.x & 0xFFFFF;
     const int qm = r_h * (spb - kSpBias - kExt) - d.t0 - (((unsigned)it.x >> 20) & 0x3FF);
     const int e = up * qm + half1;  // >= 0
@@ -935,8 +963,9 @@ __global__ void __launch_bounds__(kTailThreads) tail_kernel(const __grid_constan
       const double as = fabs((double)aes);
       straddle(qs, as, aes < 0.f ? as : 0.0);
     }
+    }
   }
-  }  // groups
+  }  // chunks
   if (clampF != 0.0 || clampE != 0.0) straddle(q_last, clampF, clampE);  // (warp-uniform)
   // boundary state s = 2 Re(v0 zeta) and the corrections of outputs n_c + lane
   Cplx zF = {z.x, z.y}, zE = {z.z, z.w};
@@ -981,7 +1010,8 @@ __global__ void __launch_bounds__(kTailThreads) tail_kernel(const __grid_constan
 }
 
 static size_t tail_smem(const frir_plan_desc& d) {
-  return (size_t)(128 + d.down + d.horizon / 128 + 1) * 16 + (size_t)kTailWarps * 2 * lt_cap(d) * 8;
+  return (size_t)(128 + d.down + d.horizon / 128 + 1) * 16 + (size_t)kTailWarps * 2 * lt_cap(d) * 8 +
+         (size_t)kTailWarps * 2 * (kTailChunk + 2) * 8;
 }
 
 // ---------------------------------------------------------------- K3 render
@@ -1603,7 +1633,7 @@ int check_line() {
 }
 
 size_t workspace_bytes(const frir_batch* b) {
-  size_t n = align_up((size_t)b->total_items * 8) + raw_bytes(b) + 3 * align_up((size_t)b->total_channels * 4) +
+  size_t n = align_up((size_t)b->total_items * 8) + raw_bytes(b) + 4 * align_up((size_t)b->total_channels * 4) +
              align_up((size_t)b->total_channels * 64 * 8) + 256;
   const int smax = batch_seg_max(b);
   if (smax > 1)
