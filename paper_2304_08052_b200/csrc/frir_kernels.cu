@@ -46,6 +46,7 @@ struct Workspace {
   int* chan_tail;   // first item of the HP-horizon suffix per channel (K2 -> K2b)
   float* chan_scale;
   double* corr;     // per channel [F, E][32]: tail corrections of outputs n_c + i (K2 -> K3)
+  longlong2* chan_row;  // per channel {first item, rows} (K1 -> K2: the row's TMA load issues after one load)
   int* counter;
 };
 
@@ -93,6 +94,7 @@ Workspace carve(void* base, const frir_batch* b) {
   w.chan_tail = (int*)p; p += align_up((size_t)b->total_channels * 4);
   w.chan_scale = (float*)p; p += align_up((size_t)b->total_channels * 4);
   w.corr = (double*)p; p += align_up((size_t)b->total_channels * 64 * 8);
+  w.chan_row = (longlong2*)p; p += align_up((size_t)b->total_channels * 16);
   w.counter = (int*)p;
   return w;
 }
@@ -102,7 +104,8 @@ SegWs carve_seg(void* base, const frir_batch* b) {
   SegWs g{nullptr, nullptr, nullptr, nullptr};
   if (batch_seg_max(b) <= 1) return g;
   char* p = (char*)base + align_up((size_t)b->total_items * 8) + raw_bytes(b) +
-            4 * align_up((size_t)b->total_channels * 4) + align_up((size_t)b->total_channels * 64 * 8) + 256;
+            4 * align_up((size_t)b->total_channels * 4) + align_up((size_t)b->total_channels * 64 * 8) +
+            align_up((size_t)b->total_channels * 16) + 256;
   g.seg = (int*)p; p += align_up((size_t)b->total_channels * kSegInts * 4);
   g.state = (double*)p; p += align_up((size_t)b->total_channels * kMaxSeg * 4 * 8);
   g.units = (int*)p; p += align_up((size_t)b->total_channels * kMaxSeg * 4);
@@ -329,6 +332,7 @@ __global__ void __launch_bounds__(128, FRIR_GEOM_MINB) geom_kernel(GeomArgs A) {
       q = min(q, J.L - 1);
       items[(size_t)m * rows] = drop ? dropped_item(J.n2) : make_item(q, (float)__drcp_rn(D), A.r_h, A.t0, A.rh_magic);
       A.ws.chan_q0[J.chan_off + m] = q;
+      A.ws.chan_row[J.chan_off + m] = make_longlong2((long long)J.item_off + (long long)m * rows, rows);
       A.ws.chan_scale[J.chan_off + m] = J.normalize ? (float)D : 1.0f;  // direct path -> 1/(1 m)
       // resample.py:115-119: clip(round(q0 / r_h), 0, n2 - 1), half-even
       int di = (int)rint(__ddiv_rn((double)q, (double)A.r_h));
@@ -523,6 +527,21 @@ __global__ void __launch_bounds__(NW * 32, (K > 0 ? 1024 : 2048) / (NW * 32)) so
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_wsum[kSortWarps];
   const int c = blockIdx.x;
+  __shared__ __align__(8) unsigned long long s_bar;
+  if constexpr (K > 0) {
+    // K > 0: the raw row lands in the staging buffer by one TMA bulk copy of
+    // its 16-byte-aligned cover (lead = 0 or 1 item before the row; the cover
+    // ends at most 8 bytes past it, inside the 256-byte-aligned workspace),
+    // issued from K1's per-channel row descriptor before the job is read
+    if (threadIdx.x == 0) {
+      const longlong2 cr = A.ws.chan_row[c];
+      const uintptr_t a0 = reinterpret_cast<uintptr_t>(A.ws.items_raw + cr.x);
+      const uintptr_t g0 = a0 & ~(uintptr_t)15, g1 = (a0 + 8 * (uintptr_t)cr.y + 15) & ~(uintptr_t)15;
+      const unsigned bar = smem_u32(&s_bar);
+      mbar_init_expect(bar, (unsigned)(g1 - g0));
+      bulk_g2s(smem_u32(smem + A.stage_off), reinterpret_cast<const void*>(g0), (unsigned)(g1 - g0), bar);
+    }
+  }
   const int j = A.chan_job[c];
   const frir_job& J = A.jobs[j];
   const int m = c - J.chan_off;
@@ -540,20 +559,8 @@ __global__ void __launch_bounds__(NW * 32, (K > 0 ? 1024 : 2048) / (NW * 32)) so
   // whole 32-row groups per warp, the row held in registers)
   const int chunk = K > 0 ? (rows + kSortThreads - 1) / kSortThreads * 32 : (rows + kSortWarps - 1) / kSortWarps;
   const int r_lo = warp * chunk, r_hi = min(rows, r_lo + chunk);
-  // K > 0: the raw row lands in the staging buffer by one TMA bulk copy of
-  // its 16-byte-aligned cover (lead = 0 or 1 item before the row; the cover
-  // ends at most 8 bytes past it, inside the 256-byte-aligned workspace)
-  __shared__ __align__(8) unsigned long long s_bar;
   const uintptr_t sa = reinterpret_cast<uintptr_t>(src);
   const int lead = (int)((sa >> 3) & 1);
-  if constexpr (K > 0) {
-    if (tid == 0) {
-      const uintptr_t g0 = sa & ~(uintptr_t)15, g1 = (sa + 8 * (uintptr_t)rows + 15) & ~(uintptr_t)15;
-      const unsigned bar = smem_u32(&s_bar);
-      mbar_init_expect(bar, (unsigned)(g1 - g0));
-      bulk_g2s(smem_u32(s_sorted), reinterpret_cast<const void*>(g0), (unsigned)(g1 - g0), bar);
-    }
-  }
   const int2* s_raw = K > 0 ? s_sorted + lead : nullptr;
   for (int i = tid; i < nwords; i += kSortThreads) reinterpret_cast<unsigned*>(s_cnt)[i] = 0u;
   __syncthreads();
@@ -807,7 +814,10 @@ struct TailArgs {
 
 constexpr int kTailThreads = 128;
 constexpr int kTailWarps = kTailThreads / 32;
-constexpr int kTailChunk = 256;  // items per TMA chunk of the suffix (2 chunks in flight per warp)
+#ifndef FRIR_TAIL_CHUNK
+#define FRIR_TAIL_CHUNK 256
+#endif
+constexpr int kTailChunk = FRIR_TAIL_CHUNK;  // items per TMA chunk of the suffix (2 chunks in flight per warp)
 
 template <bool SPLIT>
 __global__ void __launch_bounds__(kTailThreads) tail_kernel(const __grid_constant__ TailArgs A) {
@@ -833,8 +843,7 @@ __global__ void __launch_bounds__(kTailThreads) tail_kernel(const __grid_constan
   if (long_chan != SPLIT) return;  // (CTA-uniform when SPLIT)
   const int j = A.chan_job[c];
   const frir_job& J = A.jobs[j];
-  const int m = c - J.chan_off;
-  const int2* items = A.ws.items + J.item_off + (size_t)m * (J.n_images + 1);
+  const int2* items = A.ws.items + A.ws.chan_row[c].x;  // (K1's row descriptor: no wait for the job)
   const int rows = A.ws.chan_rows[c];  // sorted items before the dropped-arrival bucket
   const int n1 = J.n1, n2 = J.n2;
   const int up = d.up, down = d.down, half1 = d.half1, r_h = d.r_h;
@@ -1586,6 +1595,7 @@ __global__ void __launch_bounds__(kTrainThreads) train_items_kernel(const double
     s_base = 0;
     ws.chan_q0[c] = 0;
     ws.chan_scale[c] = 1.0f;
+    ws.chan_row[c] = make_longlong2((long long)J.item_off + (long long)m * rows, rows);
   }
   __syncthreads();
   for (int n0 = 0; n0 < L; n0 += kTrainThreads) {
@@ -1634,7 +1644,7 @@ int check_line() {
 
 size_t workspace_bytes(const frir_batch* b) {
   size_t n = align_up((size_t)b->total_items * 8) + raw_bytes(b) + 4 * align_up((size_t)b->total_channels * 4) +
-             align_up((size_t)b->total_channels * 64 * 8) + 256;
+             align_up((size_t)b->total_channels * 64 * 8) + align_up((size_t)b->total_channels * 16) + 256;
   const int smax = batch_seg_max(b);
   if (smax > 1)
     n += align_up((size_t)b->total_channels * kSegInts * 4) + align_up((size_t)b->total_channels * kMaxSeg * 4 * 8) +
