@@ -190,6 +190,8 @@ int frir_jobs_prepare(int32_t sample_rate, frir_job* jobs_host, int32_t n_jobs,
 size_t frir_workspace_size(const frir_plan* plan, const frir_batch* batch);
 
 /* Render every job of the batch: full (and, if out_early != NULL, early) RIRs.
+   `workspace` must be 256-byte aligned and the outputs 16-byte aligned (any
+   cudaMalloc'd buffer is); otherwise FRIR_EINVAL.
    Replaces core.py:131-265 (sampling, delays, train, early window) and
    resample.py:81-136 (both decimation stages and the HP).  direct_index gets
    RirFilter.direct_path_sample per channel (resample.py:115-119).  Draws come

@@ -412,6 +412,12 @@ int frir_simulate_stages(const frir_plan* plan, const frir_batch* b, void* ws, s
     return FRIR_EINVAL;
   }
   if (stages <= 0 || stages > FRIR_STAGE_ALL) { set_error("bad stage mask"); return FRIR_EINVAL; }
+  // TMA bulk copies and float4 row stores: a cudaMalloc'd (256-byte aligned)
+  // workspace and 16-byte aligned output buffers
+  if (((uintptr_t)ws & 255) || ((uintptr_t)out_full & 15) || ((uintptr_t)out_early & 15)) {
+    set_error("workspace must be 256-byte aligned and outputs 16-byte aligned (cudaMalloc'd buffers)");
+    return FRIR_EINVAL;
+  }
   const bool oracle = b->draw_dist || b->draw_az || b->draw_el || b->draw_refl;
   if (oracle && !(b->draw_dist && b->draw_az && b->draw_el && b->draw_refl)) {
     set_error("oracle mode needs all four draw arrays");
