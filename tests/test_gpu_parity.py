@@ -518,6 +518,28 @@ def test_empty_batch_is_a_no_op():
     assert res.full.numel() == 0 and res.early.numel() == 0 and res.direct_index.numel() == 0
 
 
+def test_misaligned_buffers_rejected():
+    """frir_simulate's TMA copies and float4 row stores need a 256-byte
+    aligned workspace and 16-byte aligned outputs: others are refused with
+    FRIR_EINVAL and a message, before any launch."""
+    import ctypes
+
+    from paper_2304_08052_b200 import _abi
+
+    w = workloads.config2(2)
+    db = engine.DeviceBatch(engine.prepare(16000, w.jobs, w.mics))
+    full, early, direct = db.alloc_outputs(True)
+    lib = _abi.lib()
+    st = torch.cuda.current_stream().cuda_stream
+    for ws_off, out_off in ((8, 0), (0, 4)):
+        status = lib.frir_simulate(db.plan.handle, ctypes.byref(db.batch), db.workspace.data_ptr() + ws_off,
+                                   db.workspace_bytes, full.data_ptr() + out_off, early.data_ptr(),
+                                   direct.data_ptr(), st)
+        assert status == _abi.FRIR_EINVAL and "aligned" in _abi.last_error()
+    db.launch(full, early, direct)  # the aligned call still works
+    torch.cuda.synchronize()
+
+
 def test_dropin_calls_from_threads_match_sequential():
     """The drop-in path reuses per-(rate, device) buffers (engine.CallRunner);
     concurrent callers serialise on its lock and get their own results."""
