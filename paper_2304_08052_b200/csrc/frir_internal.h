@@ -59,6 +59,7 @@ struct LaunchCache {
   int sms = 148;
   int smem_optin = 227 * 1024;  // max dynamic smem per block (opt-in)
   int render_per_sm[2][2][2] = {};  // [EARLY][NBK - 1][SEG]: resident render CTAs per SM
+  int render_e_per_sm[2] = {};      // [NBK - 1]: the early pass
 };
 
 }  // namespace frir

@@ -44,6 +44,7 @@ struct Workspace {
   int* chan_q0;
   int* chan_rows;   // items per channel before the dropped-arrival bucket (K2 -> K2b, K3)
   int* chan_tail;   // first item of the HP-horizon suffix per channel (K2 -> K2b)
+  int2* chan_erange; // items [x, y): the buckets that hold the channel's early items (K2 -> K3 early pass)
   float* chan_scale;
   double* corr;     // per channel [F, E][32]: tail corrections of outputs n_c + i (K2 -> K3)
   longlong2* chan_row;  // per channel {first item, rows} (K1 -> K2: the row's TMA load issues after one load)
@@ -92,6 +93,7 @@ Workspace carve(void* base, const frir_batch* b) {
   w.chan_q0 = (int*)p; p += align_up((size_t)b->total_channels * 4);
   w.chan_rows = (int*)p; p += align_up((size_t)b->total_channels * 4);
   w.chan_tail = (int*)p; p += align_up((size_t)b->total_channels * 4);
+  w.chan_erange = (int2*)p; p += align_up((size_t)b->total_channels * 8);
   w.chan_scale = (float*)p; p += align_up((size_t)b->total_channels * 4);
   w.corr = (double*)p; p += align_up((size_t)b->total_channels * 64 * 8);
   w.chan_row = (longlong2*)p; p += align_up((size_t)b->total_channels * 16);
@@ -104,8 +106,8 @@ SegWs carve_seg(void* base, const frir_batch* b) {
   SegWs g{nullptr, nullptr, nullptr, nullptr};
   if (batch_seg_max(b) <= 1) return g;
   char* p = (char*)base + align_up((size_t)b->total_items * 8) + raw_bytes(b) +
-            4 * align_up((size_t)b->total_channels * 4) + align_up((size_t)b->total_channels * 64 * 8) +
-            align_up((size_t)b->total_channels * 16) + 256;
+            4 * align_up((size_t)b->total_channels * 4) + align_up((size_t)b->total_channels * 8) +
+            align_up((size_t)b->total_channels * 64 * 8) + align_up((size_t)b->total_channels * 16) + 256;
   g.seg = (int*)p; p += align_up((size_t)b->total_channels * kSegInts * 4);
   g.state = (double*)p; p += align_up((size_t)b->total_channels * kMaxSeg * 4 * 8);
   g.units = (int*)p; p += align_up((size_t)b->total_channels * kMaxSeg * 4);
@@ -563,6 +565,30 @@ __global__ void __launch_bounds__(NW * 32, (K > 0 ? 1024 : 2048) / (NW * 32)) so
   const int lead = (int)((sa >> 3) & 1);
   const int2* s_raw = K > 0 ? s_sorted + lead : nullptr;
   for (int i = tid; i < nwords; i += kSortThreads) reinterpret_cast<unsigned*>(s_cnt)[i] = 0u;
+  // Buckets whose starts the later kernels need, found by thread 0 while the
+  // row loads (the scan writes the starts): K2b's HP-horizon suffix begins at
+  // the first bucket whose items can feed the state at n1 (k_hi >= n1 -
+  // horizon; bucket b bounds q by qmax(b)); the render's early pass reads the
+  // buckets of the early items (q in [q0 - e_lo, q0 + e_hi], core.py:257-264).
+  __shared__ int s_mark[3];  // [suffix start, first early bucket, one past the last] (<= nbk - 1)
+  if (tid == 0) {
+    const frir_plan_desc& d = A.plan.d;
+    const long long kthr = (long long)J.n1 - d.horizon;
+    int lo = 0, hi = nbk - 1;  // smallest b not below the horizon (nbk - 1: none)
+    while (kthr > 0 && lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      const long long qmax = (long long)d.r_h * ((mid << 5) + 31 - kSpBias - kExt) - d.t0;
+      if ((long long)d.up * qmax + d.half1 < kthr * d.down) lo = mid + 1; else hi = mid;
+    }
+    auto bucket_of = [&](int q) {  // as make_item computes it
+      const int sq = (q + d.t0 + 64 * d.r_h + d.r_h - 1) / d.r_h - 64;  // ceil((q + t0) / r_h), q >= 0
+      return (sq + kExt + kSpBias) >> 5;
+    };
+    const int q0 = A.ws.chan_q0[c];
+    s_mark[0] = lo;
+    s_mark[1] = min(bucket_of(max(q0 - J.e_lo, 0)), nbk - 1);
+    s_mark[2] = min(bucket_of(min(q0 + J.e_hi, J.L - 1)) + 1, nbk - 1);
+  }
   __syncthreads();
   if constexpr (K > 0) {
     mbar_wait(smem_u32(&s_bar), 0);
@@ -609,6 +635,9 @@ __global__ void __launch_bounds__(NW * 32, (K > 0 ? 1024 : 2048) / (NW * 32)) so
       if (lane >= o) wi += v;
     }
     int run = carry + inc - tot + __shfl_sync(0xffffffffu, wi - ws, warp);
+    if (b == s_mark[0]) A.ws.chan_tail[c] = run;  // (bucket b starts at item `run`)
+    if (b == s_mark[1]) A.ws.chan_erange[c].x = run;
+    if (b == s_mark[2]) A.ws.chan_erange[c].y = run;
     const int all = __shfl_sync(0xffffffffu, wi, kSortWarps - 1);
     if (b < nbk) {
 #pragma unroll
@@ -628,26 +657,7 @@ __global__ void __launch_bounds__(NW * 32, (K > 0 ? 1024 : 2048) / (NW * 32)) so
     __syncthreads();
   }
   const int nvalid = (int)s_cnt[cnt_idx<CT>(nbk - 1, 0, nbk)];  // items before the dropped-arrival bucket
-  if (tid == 0) {
-    A.ws.chan_rows[c] = nvalid;
-    // K2b's HP-horizon suffix starts at the first bucket whose items can feed
-    // the state at n1 (k_hi >= n1 - horizon; bucket b bounds q by qmax(b)).
-    // Counter (b, warp 0) is bucket b's start; only warp 0 advances it.
-    const frir_plan_desc& d = A.plan.d;
-    const long long kthr = (long long)J.n1 - d.horizon;
-    int p_t = 0;
-    if (kthr > 0) {
-      int lo = 0, hi = nbk - 1;  // smallest b not below the horizon (nbk - 1: none)
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        const long long qmax = (long long)d.r_h * ((mid << 5) + 31 - kSpBias - kExt) - d.t0;
-        if ((long long)d.up * qmax + d.half1 < kthr * d.down) lo = mid + 1; else hi = mid;
-      }
-      p_t = min((int)s_cnt[cnt_idx<CT>(lo, 0, nbk)], nvalid);
-    }
-    A.ws.chan_tail[c] = p_t;
-  }
-  __syncwarp();  // lane 0 read warp 0's counters before the scatter advances them
+  if (tid == 0) A.ws.chan_rows[c] = nvalid;
   const int S = SEG ? seg_count(nvalid, J.n2) : 1;
   if (SEG && tid == 0) A.sw.seg[(size_t)c * kSegInts + 63] = S;  // read by K3 / K4
   if (S > 1) {
@@ -1188,8 +1198,14 @@ struct Channel {
   }
 };
 
-template <bool EARLY, int NBK, bool SEG>  // SEG: the batch may hold segmented channels
+// SEG: the batch may hold segmented channels.  EONLY (with EARLY = false,
+// SEG = false): the early pass -- the early variant alone, from the items of
+// the buckets K2 marked (chan_erange), with the full variant's machinery: the
+// same sums in the same order as a full + early sweep (identical bits), while
+// the full pass (EARLY = false) carries no early work in its item loop.
+template <bool EARLY, int NBK, bool SEG, bool EONLY = false>
 __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(const __grid_constant__ RenderArgs A) {
+  static_assert(!EONLY || (!EARLY && !SEG), "the early pass: unsegmented channels, one variant");
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_stidx[kWarps];
   const frir_plan_desc& d = A.plan.d;
@@ -1226,10 +1242,11 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(const __grid_
     // work unit v: first the later segments of long channels (K2's list, the
     // longest work), then the first segment of every channel, longest first
     int v = 0;
-    if (lane == 0) v = atomicAdd(A.ws.counter, 1);
+    if (lane == 0) v = atomicAdd(A.ws.counter + (EONLY ? 1 : 0), 1);
     v = __shfl_sync(0xffffffffu, v, 0);
     const int nextra = SEG ? *A.sw.nextra : 0;
     int c, sg = 0;
+    constexpr bool eonly = EONLY;
     if (v < nextra) {
       const int u = A.sw.units[v];
       c = u / kMaxSeg;
@@ -1250,13 +1267,13 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(const __grid_
     const double scale = (double)A.ws.chan_scale[c];
     const int2* items = A.ws.items + J.item_off + (size_t)m * rows;
     const int nvalid = A.ws.chan_rows[c];  // sorted items before the dropped-arrival bucket
-    float* outF = A.out_full + J.out_off + (size_t)m * J.out_stride;
+    float* outF = (eonly ? A.out_early : A.out_full) + J.out_off + (size_t)m * J.out_stride;  // (eonly: early)
     float* outE = EARLY ? A.out_early + J.out_off + (size_t)m * J.out_stride : nullptr;
 
     const int n_c = first_corrected(d, n1);  // outputs n >= n_c get K2's tail corrections
     // windows touched by early items (q in [q0 - lo, q0 + hi], core.py:257-264)
     int ew_lo = 0, ew_hi = -1;
-    if (EARLY) {
+    if (EARLY || EONLY) {
       const int q0 = A.ws.chan_q0[c];
       ew_lo = (ceil_div_i(q0 - J.e_lo + d.t0, r_h) + kExt) >> 5;
       ew_hi = (ceil_div_i(q0 + J.e_hi + d.t0, r_h) + kExt + sup - 1) >> 5;
@@ -1296,8 +1313,10 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(const __grid_
               if (idx >= 0 && idx < d.len2) cd += cc * A.plan.h2[idx];
               if (idx >= 0 && idx < d.len2 + 2 * d.r_l) cw += cc * A.plan.gw[idx];
             }
-            head_s[np] -= (float)cd;
-            head_s[64 + np] -= (float)cw;
+            if (!eonly || aes < 0.f) {  // (the early pass: early head items only)
+              head_s[np] -= (float)cd;
+              head_s[64 + np] -= (float)cw;
+            }
             if (EARLY && aes < 0.f) {
               head_s[128 + np] -= (float)cd;
               head_s[192 + np] -= (float)cw;
@@ -1313,7 +1332,7 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(const __grid_
     }
 
     // ---- tail corrections of outputs n >= n_c (computed by K2)
-    corrF_s[lane] = A.ws.corr[64 * (size_t)c + lane];
+    corrF_s[lane] = A.ws.corr[64 * (size_t)c + (eonly ? 32 : 0) + lane];
     if (EARLY) corrE_s[lane] = A.ws.corr[64 * (size_t)c + 32 + lane];
     __syncwarp();
 
@@ -1323,6 +1342,17 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(const __grid_
     if (SEG && nseg > 1) {
       const int* seg = A.sw.seg + (size_t)c * kSegInts;
       w_lo = seg[sg]; nwin = seg[sg + 1]; i_lo = seg[17 + sg]; i_hi = seg[33 + sg];
+    }
+    if (eonly) {  // the early pass: the buckets of the early items; the tiles before them are zeros
+      const int2 er = A.ws.chan_erange[c];
+      i_lo = er.x;
+      i_hi = er.y;
+      if (i_lo < i_hi && !head_on) {  // (q0 itself is early, so the range is never empty)
+        const int b_first = (items[i_lo].x & 0xFFFFF) >> 5;  // feeds windows b_first - 2 ..
+        w_lo = max(0, (b_first - 2) & ~(kTileWin - 1));
+      }
+      const int pre = min(nrow, w_lo * kWin - kExt);  // (a multiple of 4)
+      for (int n = 4 * lane; n < pre; n += 128) *reinterpret_cast<float4*>(outF + n) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 
     Channel<EARLY, NBK> ch;
@@ -1354,38 +1384,46 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(const __grid_
       }
       __syncwarp();
       double lp[kChunk];
-      lp_scan_tile(wF_t, A.plan, c1, c2, sF0, sF1, lane, lp);
-      store_chunk(outF, n_base, n2, nrow, n_c, dF_t, corrF_s, lane, lp, scale);
-      if (EARLY) {
+      // the early variant's tile: scanned while early items feed it, then the
+      // closed-form decay of its LP state, then zeros
+      auto early_tile = [&](float* out, const float* d_t, const float* w_t, const double* corr_s, double& s0,
+                            double& s1) {
         const bool quiet = w0 > ew_hi;  // no early item feeds this tile: pure decay
         if (!quiet) {
-          lp_scan_tile(wE_t, A.plan, c1, c2, sE0, sE1, lane, lp);
-          store_chunk(outE, n_base, n2, nrow, n_c, dE_t, corrE_s, lane, lp, scale);
-          e_ref = fmax(e_ref, fabs(sE0) + fabs(sE1));
+          lp_scan_tile(w_t, A.plan, c1, c2, s0, s1, lane, lp);
+          store_chunk(out, n_base, n2, nrow, n_c, d_t, corr_s, lane, lp, scale);
+          e_ref = fmax(e_ref, fabs(s0) + fabs(s1));
         } else if (!e_dead) {
           // LP[k] = row0(M^(k+1)) . s for the whole tile; y = -LP (D = W = 0)
           const double* fr = A.plan.scan + kScanFree + 2 * kChunk * lane;  // global (L1)
 #pragma unroll
-          for (int k = 0; k < kChunk; ++k) lp[k] = fma(fr[2 * k], sE0, fr[2 * k + 1] * sE1);
+          for (int k = 0; k < kChunk; ++k) lp[k] = fma(fr[2 * k], s0, fr[2 * k + 1] * s1);
           const double* Mt = A.plan.mt;
-          const double n0v = fma(Mt[0], sE0, Mt[1] * sE1), n1v = fma(Mt[2], sE0, Mt[3] * sE1);
-          sE0 = n0v;
-          sE1 = n1v;
-          store_chunk<false>(outE, n_base, n2, nrow, n_c, dE_t, corrE_s, lane, lp, scale);
+          const double n0v = fma(Mt[0], s0, Mt[1] * s1), n1v = fma(Mt[2], s0, Mt[3] * s1);
+          s0 = n0v;
+          s1 = n1v;
+          store_chunk<false>(out, n_base, n2, nrow, n_c, d_t, corr_s, lane, lp, scale);
           // the ring-down after the early window decays by ~0.06 per tile at
           // 16 kHz; once |s| < 2^-44 of its early-window maximum, the rest
           // (|LP| <= ~400 |s|) is below 1e-10 of the channel's level
-          e_dead = fabs(sE0) + fabs(sE1) < fmax(1e-50, 0x1p-44 * e_ref);
+          e_dead = fabs(s0) + fabs(s1) < fmax(1e-50, 0x1p-44 * e_ref);
         } else {
           const int n0 = n_base + kChunk * lane;
           if (n0 >= 0 && n0 + kChunk <= nrow) {  // (rows are 16-byte aligned, n_base % 4 == 0)
-            *reinterpret_cast<float4*>(outE + n0) = make_float4(0.f, 0.f, 0.f, 0.f);
+            *reinterpret_cast<float4*>(out + n0) = make_float4(0.f, 0.f, 0.f, 0.f);
           } else {
 #pragma unroll
             for (int k = 0; k < kChunk; ++k)
-              if (n0 + k >= 0 && n0 + k < nrow) outE[n0 + k] = 0.f;
+              if (n0 + k >= 0 && n0 + k < nrow) out[n0 + k] = 0.f;
           }
         }
+      };
+      if (eonly) {
+        early_tile(outF, dF_t, wF_t, corrF_s, sF0, sF1);
+      } else {
+        lp_scan_tile(wF_t, A.plan, c1, c2, sF0, sF1, lane, lp);
+        store_chunk(outF, n_base, n2, nrow, n_c, dF_t, corrF_s, lane, lp, scale);
+        if (EARLY) early_tile(outE, dE_t, wE_t, corrE_s, sE0, sE1);
       }
       if (SEG && w == nwin - 1 && lane == 0) {  // last tile of the sweep: zero-start end state of a segment (K4)
         const int si = s_stidx[warp];
@@ -1422,7 +1460,7 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(const __grid_
       const unsigned dec = (((unsigned)mine.x >> 20) & 0x3FFu) * (512u * NBK) + 8u * (32u - (mine.x & 31));
       FRIR_CHECK(p + lane >= srows || (((unsigned)mine.x >> 20) & 0x3FFu) < (unsigned)r_h);
       __syncwarp();
-      s_it[lane] = make_int2((int)dec, mine.y);
+      s_it[lane] = make_int2((int)dec, eonly && mine.y >= 0 ? 0 : mine.y);  // (early pass: late items add +0)
       __syncwarp();
       const int cnt = min(32, srows - p);
       const unsigned emask = EARLY ? __ballot_sync(0xffffffffu, lane < cnt && mine.y < 0) : 0u;
@@ -1447,7 +1485,30 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(const __grid_
         }
       }
     }
-    while (w < nwin) emit();
+    if (eonly) {
+      // the tiles early items feed go through the sweep; the quiet ones after
+      // them need no windows: the closed-form decay of the LP state tile by
+      // tile (as early_tile does), then zeros to the end of the row
+      while (w < nwin && !(slot == 0 && w > ew_hi)) emit();
+      for (; w < nwin && !e_dead; w += kTileWin) {
+        const int n_base = w * kWin - kExt;
+        double lp[kChunk];
+        const double* fr = A.plan.scan + kScanFree + 2 * kChunk * lane;  // global (L1)
+#pragma unroll
+        for (int k = 0; k < kChunk; ++k) lp[k] = fma(fr[2 * k], sF0, fr[2 * k + 1] * sF1);
+        const double* Mt = A.plan.mt;
+        const double n0v = fma(Mt[0], sF0, Mt[1] * sF1), n1v = fma(Mt[2], sF0, Mt[3] * sF1);
+        sF0 = n0v;
+        sF1 = n1v;
+        store_chunk<false>(outF, n_base, n2, nrow, n_c, dF_t, corrF_s, lane, lp, scale);
+        e_dead = fabs(sF0) + fabs(sF1) < fmax(1e-50, 0x1p-44 * e_ref);
+      }
+      const int n_from = max(0, w * kWin - kExt);  // first output of tile w
+      if (w < nwin)
+        for (int n = n_from + 4 * lane; n < nrow; n += 128) *reinterpret_cast<float4*>(outF + n) = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      while (w < nwin) emit();
+    }
   }
 }
 
@@ -1644,7 +1705,8 @@ int check_line() {
 
 size_t workspace_bytes(const frir_batch* b) {
   size_t n = align_up((size_t)b->total_items * 8) + raw_bytes(b) + 4 * align_up((size_t)b->total_channels * 4) +
-             align_up((size_t)b->total_channels * 64 * 8) + align_up((size_t)b->total_channels * 16) + 256;
+             align_up((size_t)b->total_channels * 8) + align_up((size_t)b->total_channels * 64 * 8) +
+             align_up((size_t)b->total_channels * 16) + 256;
   const int smax = batch_seg_max(b);
   if (smax > 1)
     n += align_up((size_t)b->total_channels * kSegInts * 4) + align_up((size_t)b->total_channels * kMaxSeg * 4 * 8) +
@@ -1675,11 +1737,11 @@ static cudaError_t allow_smem(K k, int optin) {
 // Every kernel that takes dynamic shared memory gets the device's opt-in
 // maximum once here, and the render kernels' residency is queried once, so a
 // launch issues no attribute or occupancy calls (plan = one device).
-template <bool EARLY, int NBK, bool SEG>
+template <bool EARLY, int NBK, bool SEG, bool EONLY = false>
 static cudaError_t init_render(frir_plan* p) {
-  auto k = render_kernel<EARLY, NBK, SEG>;
+  auto k = render_kernel<EARLY, NBK, SEG, EONLY>;
   const size_t smem = render_smem(p->dev.d, EARLY);
-  int& per_sm = p->lc.render_per_sm[EARLY][NBK - 1][SEG];
+  int& per_sm = EONLY ? p->lc.render_e_per_sm[NBK - 1] : p->lc.render_per_sm[EARLY][NBK - 1][SEG];
   per_sm = 0;
   if ((int)smem > p->lc.smem_optin - kDynSlack) return cudaSuccess;  // 0: this plan cannot launch it
   // the cap is per kernel, not per plan: plans of other rates launch it with other sizes
@@ -1716,25 +1778,35 @@ cudaError_t init_launch_cache(frir_plan* p) {
   if (e == cudaSuccess) e = init_render<true, 2, true>(p);
   if (e == cudaSuccess) e = init_render<false, 2, false>(p);
   if (e == cudaSuccess) e = init_render<false, 2, true>(p);
+  if (e == cudaSuccess) e = init_render<false, 1, false, true>(p);
+  if (e == cudaSuccess) e = init_render<false, 2, false, true>(p);
   return e;
 }
 
-template <bool EARLY, int NBK, bool SEG>
+template <bool EARLY, int NBK, bool SEG, bool EONLY = false>
 static cudaError_t launch_render(const frir_plan* plan, const RenderArgs& ra, long channels, cudaStream_t st) {
   const size_t smem = render_smem(plan->dev.d, EARLY);
-  const int per_sm = plan->lc.render_per_sm[EARLY][NBK - 1][SEG];
+  const int per_sm = EONLY ? plan->lc.render_e_per_sm[NBK - 1] : plan->lc.render_per_sm[EARLY][NBK - 1][SEG];
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   long want = (channels * ra.seg_max + kWarps - 1) / kWarps;  // upper bound of the work units
   int grid = (int)std::min<long>((long)plan->lc.sms * per_sm, want);
-  render_kernel<EARLY, NBK, SEG><<<grid, kRenderThreads, smem, st>>>(ra);
+  render_kernel<EARLY, NBK, SEG, EONLY><<<grid, kRenderThreads, smem, st>>>(ra);
   return cudaGetLastError();
 }
 
+#ifndef FRIR_SPLIT_EARLY_CHANNELS
+#define FRIR_SPLIT_EARLY_CHANNELS 12288
+#endif
+constexpr long kSplitEarlyChannels = FRIR_SPLIT_EARLY_CHANNELS;
+static bool split_early(const frir_batch* b) {
+  return batch_seg_max(b) <= 1 && (long)b->total_channels >= kSplitEarlyChannels;
+}
+
 int launches(const frir_batch* b, int early) {
-  (void)early;
-  // geom, sort, tail, render (plus one memset of the work counter); the split
-  // tail and the seam kernel when the batch may hold segmented (long) channels
-  return 4 + (batch_seg_max(b) > 1 ? 2 : 0);
+  // geom, sort, tail, render (plus one memset of the work counters); the split
+  // tail and the seam kernel when the batch may hold segmented (long) channels;
+  // the early pass when it is split from the full one
+  return 4 + (batch_seg_max(b) > 1 ? 2 : 0) + (early && split_early(b) ? 1 : 0);
 }
 
 int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_t ws_bytes,
@@ -1833,7 +1905,7 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_
   }
 
   if (stages & FRIR_STAGE_RENDER) {  // K3
-    e = cudaMemsetAsync(ws.counter, 0, sizeof(int), st);
+    e = cudaMemsetAsync(ws.counter, 0, 2 * sizeof(int), st);  // [full / both, early pass]
     if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FRIR_ECUDA; }
     RenderArgs ra;
     ra.jobs = b->jobs; ra.chan_job = b->chan_job; ra.chan_order = b->chan_order;
@@ -1844,12 +1916,22 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_
     const int nbk = table_blocks(d);
     const bool seg = ra.seg_max > 1;
     const long ch = b->total_channels;
+    // batches of >= kSplitEarlyChannels channels without segmented ones
+    // render the full variant and then the early variant in a second pass over
+    // the early buckets only (identical bits to one full + early sweep; render
+    // -4% on config 5, -6% config 3, -10% config 4; +3% on config 2's 6,144
+    // channels, where the early pass cannot fill the GPU); other batches sweep
+    // both variants at once
+    const bool split = early && split_early(b);
+    const bool both = early && !split;
     if (nbk == 1)
-      e = early ? (seg ? launch_render<true, 1, true>(plan, ra, ch, st) : launch_render<true, 1, false>(plan, ra, ch, st))
-                : (seg ? launch_render<false, 1, true>(plan, ra, ch, st) : launch_render<false, 1, false>(plan, ra, ch, st));
+      e = both ? (seg ? launch_render<true, 1, true>(plan, ra, ch, st) : launch_render<true, 1, false>(plan, ra, ch, st))
+               : (seg ? launch_render<false, 1, true>(plan, ra, ch, st) : launch_render<false, 1, false>(plan, ra, ch, st));
     else
-      e = early ? (seg ? launch_render<true, 2, true>(plan, ra, ch, st) : launch_render<true, 2, false>(plan, ra, ch, st))
-                : (seg ? launch_render<false, 2, true>(plan, ra, ch, st) : launch_render<false, 2, false>(plan, ra, ch, st));
+      e = both ? (seg ? launch_render<true, 2, true>(plan, ra, ch, st) : launch_render<true, 2, false>(plan, ra, ch, st))
+               : (seg ? launch_render<false, 2, true>(plan, ra, ch, st) : launch_render<false, 2, false>(plan, ra, ch, st));
+    if (e == cudaSuccess && split)
+      e = nbk == 1 ? launch_render<false, 1, false, true>(plan, ra, ch, st) : launch_render<false, 2, false, true>(plan, ra, ch, st);
     if (e != cudaSuccess) { set_error(std::string("render_kernel: ") + cudaGetErrorString(e)); return FRIR_ECUDA; }
     if (ra.seg_max > 1) {  // K4: seams of segmented channels
       SeamArgs sa;

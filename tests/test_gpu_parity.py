@@ -420,6 +420,9 @@ def test_segmented_channels_batch_invariant_and_reproducible():
     short = engine.simulate_jobs(16000, w.jobs, w.mics)
     for j, k in ((0, 0), (2, 2), (4, 3), (6, 5)):
         assert torch.equal(a.job_view(j), short.job_view(k))
+        # short channels of a segmented batch get one full + early sweep; alone
+        # they get the full pass and the early pass: the same bits
+        assert torch.equal(a.job_view(j, "early"), short.job_view(k, "early"))
     only = engine.simulate_jobs(16000, jobs_l, mics, include_early=False)
     assert torch.equal(only.job_view(0), alone.job_view(0))
 
