@@ -1220,6 +1220,7 @@ __global__ void __launch_bounds__(kRenderThreads, 3) render_kernel(const __grid_
   int2* s_items = reinterpret_cast<int2*>(s_tile + (size_t)kWarps * V * 2 * kTileRow);
   float* s_head = reinterpret_cast<float*>(s_items + 32 * kWarps);          // [warp][V][D, W][64]
   for (int i = threadIdx.x; i < ncomp; i += blockDim.x) s_comp[i] = A.plan.comp[i];
+  if (!EARLY && !EONLY) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the early pass may start
   __syncthreads();
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1790,8 +1791,25 @@ static cudaError_t launch_render(const frir_plan* plan, const RenderArgs& ra, lo
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   long want = (channels * ra.seg_max + kWarps - 1) / kWarps;  // upper bound of the work units
   int grid = (int)std::min<long>((long)plan->lc.sms * per_sm, want);
-  render_kernel<EARLY, NBK, SEG, EONLY><<<grid, kRenderThreads, smem, st>>>(ra);
-  return cudaGetLastError();
+  if (!EONLY) {
+    render_kernel<EARLY, NBK, SEG, EONLY><<<grid, kRenderThreads, smem, st>>>(ra);
+    return cudaGetLastError();
+  }
+  // The early pass reads only K2 / K2b outputs and writes only the early rows,
+  // so it need not wait for the full pass: a programmatic dependent launch
+  // (the full pass triggers it at its start) lets its CTAs take the SMs the
+  // full pass's CTAs leave as its work queue drains.
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kRenderThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, render_kernel<EARLY, NBK, SEG, EONLY>, ra);
 }
 
 #ifndef FRIR_SPLIT_EARLY_CHANNELS
