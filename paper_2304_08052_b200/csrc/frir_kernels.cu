@@ -359,6 +359,13 @@ __global__ void __launch_bounds__(128, FRIR_GEOM_MINB) geom_kernel(GeomArgs A) {
   }
   const int nk = live ? min(4, I - 4 * g) : 0;
   const int wrow = 4 * (g - lane) + 1;  // first row of the warp
+  // per-job constants in registers: the item stores may alias the job table
+  // for the compiler, which would reload these fields for every item
+  const int q_hi = J.L + ism - 1;  // last representable arrival (ISM: one past the train = dropped)
+  const int q_keep = J.L - 1;      // arrivals after this are dropped (ISM only)
+  const int2 drop = dropped_item(J.n2);
+  const double c0 = J.c0;
+  const double half_band = 0.5 - 2e-12 * (double)(J.L + ism);
   for (int m = 0; m < M; ++m) {
     int2* out = items + (size_t)m * rows + wrow;
     const double mx = __ldg(mics + 3 * m), my = __ldg(mics + 3 * m + 1), mz = __ldg(mics + 3 * m + 2);
@@ -375,7 +382,6 @@ __global__ void __launch_bounds__(128, FRIR_GEOM_MINB) geom_kernel(GeomArgs A) {
     // them; warp-uniform test).
     double d2[4], kc[4];
     float inv_d[4];
-    const double half_band = 0.5 - 2e-12 * (double)(J.L + ism);
     unsigned gm = 0;  // rows in the guard band
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -390,16 +396,15 @@ __global__ void __launch_bounds__(128, FRIR_GEOM_MINB) geom_kernel(GeomArgs A) {
     if (__any_sync(0xffffffffu, gm != 0u)) {
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        if ((gm >> k) & 1u) kc[k] = ceil(__dmul_rn(__ddiv_rn(__dsqrt_rn(d2[k]), J.c0), A.rate));
+        if ((gm >> k) & 1u) kc[k] = ceil(__dmul_rn(__ddiv_rn(__dsqrt_rn(d2[k]), c0), A.rate));
     }
     int2 it[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const int Lx = J.L + ism;
-      const int q = kc[k] >= (double)(Lx - 1) ? Lx - 1 : (int)kc[k];
+      const int q = min(__double2int_rz(kc[k]), q_hi);  // (kc >= 0; the conversion saturates)
       FRIR_CHECK(k >= nk || (q >= 0 && q < J.L + ism && 4 * g + 1 + k < rows));
-      it[k] = q > J.L - 1 ? dropped_item(J.n2)  // ISM only: dropped arrival
-                          : make_item(q, lg[k] * inv_d[k], A.r_h, A.t0, A.rh_magic);  // r^g / D
+      it[k] = q > q_keep ? drop  // ISM only: dropped arrival
+                         : make_item(q, lg[k] * inv_d[k], A.r_h, A.t0, A.rh_magic);  // r^g / D
     }
     __syncwarp();
 #pragma unroll
