@@ -559,3 +559,32 @@ def test_dropin_calls_from_threads_match_sequential():
             assert np.array_equal(ra.full.samples, rb.full.samples)
             assert np.array_equal(ra.early.samples, rb.early.samples)
             assert np.array_equal(ra.full.direct_path_sample, rb.full.direct_path_sample)
+
+
+def test_early_pass_split_equals_combined_sweep_and_oracle():
+    """Batches of >= 12,288 unsegmented channels render the early variant in
+    a second pass (K3e) over K2's early buckets; smaller batches sweep full +
+    early at once.  The same rooms rendered both ways give identical bits, the
+    launch count says which form ran, and sampled channels match the oracle."""
+    w = workloads.build(5, 384)  # 384 rooms x 32 mics = 12,288 channels: split
+    big = engine.simulate_jobs(w.sample_rate, w.jobs, w.mics, include_early=True)
+    pb = engine.prepare(w.sample_rate, w.jobs, w.mics)
+    db = engine.DeviceBatch(pb)
+    assert db.launch_count(True) == db.launch_count(False) + 1  # the early pass
+    for lo in range(0, 384, 96):  # 3,072 channels per batch: one full + early sweep
+        jobs, mics = engine.split_jobs(w.jobs, w.mics, lo, lo + 96)
+        part = engine.simulate_jobs(w.sample_rate, jobs, mics, include_early=True)
+        sub = engine.DeviceBatch(engine.prepare(w.sample_rate, jobs, mics))
+        assert sub.launch_count(True) == sub.launch_count(False)
+        for j in range(96):
+            assert torch.equal(big.job_view(lo + j), part.job_view(j))
+            assert torch.equal(big.job_view(lo + j, "early"), part.job_view(j, "early"))
+    for j in (0, 97, 383):  # the split form against the oracle
+        J = w.jobs[j]
+        job = P.Job(room=tuple(float(x) for x in J["room"]), mics=w.mics[J["mic_off"]: J["mic_off"] + J["n_mics"]].copy(),
+                    center=np.array(J["center"]), source=(float(J["d0"]), float(J["az"]), float(J["el"])),
+                    t60=float(J["t60"]), sample_rate=w.sample_rate, num_images=int(J["n_images"]),
+                    seed=int(J["seed"]), source_index=int(J["source_index"]))
+        full_o, early_o, direct_o = P.render(job, include_early=True)
+        assert rel_err(big.job_view(j).cpu().numpy(), full_o) <= TOL
+        assert rel_err(big.job_view(j, "early").cpu().numpy(), early_o) <= TOL
