@@ -24,8 +24,10 @@ for ci, m in enumerate(meta):
     jobs["t60"], jobs["seed"], jobs["n_images"], jobs["n_mics"] = m["t60"], m["seed"], m["num_images"], len(mics)
     for early in (True, False):
         engine.simulate_jobs(m["fs"], jobs, mics, include_early=early)
-for cfg, n in ((2, 3), (3, 1), (4, 1), (5, 1)):
+for cfg, n in ((2, 3), (3, 1), (4, 1), (5, 1), (5, 384)):  # (5, 384): 12,288 channels, the early pass
     w = workloads.build(cfg, n)
+    if n == 384:
+        w.jobs["n_images"][7] = 8192  # the longest register-staged sort rows (8,193)
     engine.simulate_jobs(w.sample_rate, w.jobs, w.mics, include_early=True, padded=(cfg == 3))
 torch.cuda.synchronize()
 from paper_2304_08052_b200 import _abi  # noqa: E402
