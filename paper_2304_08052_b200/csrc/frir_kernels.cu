@@ -426,8 +426,8 @@ __global__ void __launch_bounds__(128, FRIR_GEOM_MINB) geom_kernel(GeomArgs A) {
 struct Cplx {
   double re, im;
 };
-__device__ __forceinline__ Cplx cmul(Cplx a, Cplx b) {
-  return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
+__device__ __forceinline__ Cplx cmul(Cplx a, Cplx b) {  // (this file builds with -fmad=false: fused explicitly)
+  return {fma(a.re, b.re, -(a.im * b.im)), fma(a.re, b.im, a.im * b.re)};
 }
 
 // First output whose value needs the truncation correction (outputs whose
