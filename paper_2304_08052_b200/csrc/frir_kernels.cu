@@ -707,14 +707,18 @@ __global__ void __launch_bounds__(NW * 32, (K > 0 ? 1024 : 2048) / (NW * 32)) so
   const int q0 = A.ws.chan_q0[c];
   if constexpr (K > 0) {
     int2 reg[K];  // the warp's rows leave the buffer before the scatter rewrites it
+    // this warp's 32-row groups (warp-uniform: the loops below stop there)
+    const int ngrp = __shfl_sync(0xffffffffu, r_hi > r_lo ? (r_hi - r_lo + 31) >> 5 : 0, 0);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
+      if (k >= ngrp) break;
       const int r = r_lo + 32 * k + lane;
       reg[k] = r < r_hi ? s_raw[r] : make_int2(0, 0);
     }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < K; ++k) {
+      if (k >= ngrp) break;
       if (r_lo + 32 * k + lane < r_hi) {
         int2 it = reg[k];
         const int sp = (it.x & 0xFFFFF) - kSpBias - kExt;
