@@ -414,15 +414,16 @@ def run_ours(args):
     tot_render = float(sum(render_ms))
     tot_pre = float(sum(prerender_ms))
 
-    # ---- throughput (value): launches are independent batches.  Small ones do
-    # not fill the GPU on their own, so they run as a 2-deep pipeline: launch
-    # k + 1's latency-bound geom/sort/tail kernels on a second stream (own
-    # workspace and outputs) while launch k renders.  Launches of >= 64 K
-    # channels (configs 3 and 5) fill it: there the render's three CTAs per SM
-    # leave no room for the other stream and one stream is measured faster
-    # (config 5: 309 vs 316 ms per step), so they run back to back.  The
-    # per-launch working set (item lists + RIRs) exceeds L2.
-    depth = 1 if min(int(db.batch.total_channels) for _, _, db in batches) >= 65536 else 2
+    # ---- throughput (value): launches are independent batches, run as a
+    # 2-deep pipeline: launch k + 1's latency-bound geom/sort/tail kernels on a
+    # second stream (own workspace and outputs) while launch k renders.  Small
+    # launches do not fill the GPU on their own (config 2: 1.30 -> 1.46 M
+    # RIR/s); for large ones the full render pass leaves room on each SM for a
+    # geom or tail CTA (config 5: 252.8 vs 251.0 K RIR/s on one stream,
+    # config 3 +0.3%; with round 2's first combined render, whose three CTAs
+    # filled the SMs' shared memory, one stream was faster).  The per-launch
+    # working set (item lists + RIRs) exceeds L2.
+    depth = args.value_streams or 2
     outs = [(full, earlyb, direct)]
     if depth == 2:
         outs.append((torch.empty_like(full), torch.empty_like(earlyb) if early else None, torch.empty_like(direct)))
@@ -663,6 +664,8 @@ def main():
     ap.add_argument("--config", type=int, default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--rooms", type=int, default=None, help="rooms per GPU (cfg 5: total)")
     ap.add_argument("--chunk", type=int, default=None, help="cfg 5 rooms per launch (default 4096)")
+    ap.add_argument("--value-streams", type=int, default=None, choices=[1, 2],
+                    help="streams of the throughput loop (default 2: a 2-deep pipeline of launches)")
     ap.add_argument("--e2e-part", type=int, default=None, help="jobs per part of the e2e stream")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-early", action="store_true")
