@@ -561,6 +561,32 @@ def test_dropin_calls_from_threads_match_sequential():
             assert np.array_equal(ra.full.direct_path_sample, rb.full.direct_path_sample)
 
 
+def test_early_pass_split_edge_rows():
+    """The early pass and the register-staged sort at their edges: a split
+    batch (>= 12,288 channels) whose rooms have no images at all (one item per
+    channel: the direct path) or the longest config-5 rows (8,193 items),
+    against the same rooms in combined sweeps and against the oracle."""
+    w = workloads.build(5, 384)
+    w.jobs["n_images"][:128] = 0
+    w.jobs["n_images"][128:256] = 8192
+    big = engine.simulate_jobs(w.sample_rate, w.jobs, w.mics, include_early=True)
+    for lo in (0, 128, 256):
+        jobs, mics = engine.split_jobs(w.jobs, w.mics, lo, lo + 128)
+        part = engine.simulate_jobs(w.sample_rate, jobs, mics, include_early=True)  # 4,096 channels: combined
+        for j in range(128):
+            assert torch.equal(big.job_view(lo + j), part.job_view(j))
+            assert torch.equal(big.job_view(lo + j, "early"), part.job_view(j, "early"))
+    for j in (5, 130):
+        J = w.jobs[j]
+        job = P.Job(room=tuple(float(x) for x in J["room"]), mics=w.mics[J["mic_off"]: J["mic_off"] + J["n_mics"]].copy(),
+                    center=np.array(J["center"]), source=(float(J["d0"]), float(J["az"]), float(J["el"])),
+                    t60=float(J["t60"]), sample_rate=w.sample_rate, num_images=int(J["n_images"]),
+                    seed=int(J["seed"]), source_index=int(J["source_index"]))
+        full_o, early_o, _ = P.render(job, include_early=True)
+        assert rel_err(big.job_view(j).cpu().numpy(), full_o) <= TOL
+        assert rel_err(big.job_view(j, "early").cpu().numpy(), early_o) <= TOL
+
+
 def test_early_pass_split_equals_combined_sweep_and_oracle():
     """Batches of >= 12,288 unsegmented channels render the early variant in
     a second pass (K3e) over K2's early buckets; smaller batches sweep full +
