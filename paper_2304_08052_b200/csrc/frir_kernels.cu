@@ -1822,7 +1822,7 @@ static cudaError_t launch_render(const frir_plan* plan, const RenderArgs& ra, lo
 }
 
 #ifndef FRIR_SPLIT_EARLY_CHANNELS
-#define FRIR_SPLIT_EARLY_CHANNELS 12288
+#define FRIR_SPLIT_EARLY_CHANNELS 1024
 #endif
 constexpr long kSplitEarlyChannels = FRIR_SPLIT_EARLY_CHANNELS;
 static bool split_early(const frir_batch* b) {
@@ -1946,9 +1946,10 @@ int launch_simulate(const frir_plan* plan, const frir_batch* b, void* wsp, size_
     // batches of >= kSplitEarlyChannels channels without segmented ones
     // render the full variant and then the early variant in a second pass over
     // the early buckets only (identical bits to one full + early sweep; render
-    // -4% on config 5, -6% config 3, -10% config 4; +3% on config 2's 6,144
-    // channels, where the early pass cannot fill the GPU); other batches sweep
-    // both variants at once
+    // -4% on config 5, -6% config 3, -10% config 4; config 2's 6,144-channel
+    // launches: +3% alone on one stream, but +2.2% throughput in the 2-deep
+    // launch pipeline, where the early pass overlaps the other stream's work);
+    // smaller batches (the per-call drop-in) sweep both variants at once
     const bool split = early && split_early(b);
     const bool both = early && !split;
     if (nbk == 1)

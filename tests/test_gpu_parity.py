@@ -563,17 +563,17 @@ def test_dropin_calls_from_threads_match_sequential():
 
 def test_early_pass_split_edge_rows():
     """The early pass and the register-staged sort at their edges: a split
-    batch (>= 12,288 channels) whose rooms have no images at all (one item per
+    batch (>= 1,024 channels) whose rooms have no images at all (one item per
     channel: the direct path) or the longest config-5 rows (8,193 items),
     against the same rooms in combined sweeps and against the oracle."""
     w = workloads.build(5, 384)
     w.jobs["n_images"][:128] = 0
     w.jobs["n_images"][128:256] = 8192
     big = engine.simulate_jobs(w.sample_rate, w.jobs, w.mics, include_early=True)
-    for lo in (0, 128, 256):
-        jobs, mics = engine.split_jobs(w.jobs, w.mics, lo, lo + 128)
-        part = engine.simulate_jobs(w.sample_rate, jobs, mics, include_early=True)  # 4,096 channels: combined
-        for j in range(128):
+    for lo in (0, 24, 128, 152, 256, 280):
+        jobs, mics = engine.split_jobs(w.jobs, w.mics, lo, lo + 24)
+        part = engine.simulate_jobs(w.sample_rate, jobs, mics, include_early=True)  # 768 channels: combined
+        for j in range(24):
             assert torch.equal(big.job_view(lo + j), part.job_view(j))
             assert torch.equal(big.job_view(lo + j, "early"), part.job_view(j, "early"))
     for j in (5, 130):
@@ -588,7 +588,7 @@ def test_early_pass_split_edge_rows():
 
 
 def test_early_pass_split_equals_combined_sweep_and_oracle():
-    """Batches of >= 12,288 unsegmented channels render the early variant in
+    """Batches of >= 1,024 unsegmented channels render the early variant in
     a second pass (K3e) over K2's early buckets; smaller batches sweep full +
     early at once.  The same rooms rendered both ways give identical bits, the
     launch count says which form ran, and sampled channels match the oracle."""
@@ -597,12 +597,12 @@ def test_early_pass_split_equals_combined_sweep_and_oracle():
     pb = engine.prepare(w.sample_rate, w.jobs, w.mics)
     db = engine.DeviceBatch(pb)
     assert db.launch_count(True) == db.launch_count(False) + 1  # the early pass
-    for lo in range(0, 384, 96):  # 3,072 channels per batch: one full + early sweep
-        jobs, mics = engine.split_jobs(w.jobs, w.mics, lo, lo + 96)
+    for lo in range(0, 384, 24):  # 768 channels per batch: one full + early sweep
+        jobs, mics = engine.split_jobs(w.jobs, w.mics, lo, lo + 24)
         part = engine.simulate_jobs(w.sample_rate, jobs, mics, include_early=True)
         sub = engine.DeviceBatch(engine.prepare(w.sample_rate, jobs, mics))
         assert sub.launch_count(True) == sub.launch_count(False)
-        for j in range(96):
+        for j in range(24):
             assert torch.equal(big.job_view(lo + j), part.job_view(j))
             assert torch.equal(big.job_view(lo + j, "early"), part.job_view(j, "early"))
     for j in (0, 97, 383):  # the split form against the oracle
