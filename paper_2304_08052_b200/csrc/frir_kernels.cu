@@ -6,10 +6,14 @@
 //                                                             core.py:131-251
 //   K2 sort_kernel    per channel: early flags, stable two-pass counting sort
 //                     of the items by 32-sample output window core.py:254-265
+//   K2b tail_kernel   per channel: the exact corrections of the reference's
+//                     truncation of the mid-rate signal    resample.py:107-113
 //   K3 render_kernel  persistent warps, one channel at a time: gather the
 //                     composite decimation/low-pass tables into 32-sample
 //                     windows (FP32), FP64 output-rate LP scan, exact tail
-//                     correction, coalesced full + early stores
+//                     correction, coalesced full (+ early) stores; for
+//                     batches of >= 1,024 channels the early variant is a
+//                     second pass over the early buckets only (K3e)
 //                                                             resample.py:81-136
 // No atomics touch sample values, so outputs are bit-reproducible.
 #include <cstdlib>
