@@ -614,3 +614,30 @@ def test_early_pass_split_equals_combined_sweep_and_oracle():
         full_o, early_o, direct_o = P.render(job, include_early=True)
         assert rel_err(big.job_view(j).cpu().numpy(), full_o) <= TOL
         assert rel_err(big.job_view(j, "early").cpu().numpy(), early_o) <= TOL
+
+
+def test_early_pass_split_48k_two_block_tables():
+    """The early pass with the 48 kHz plan (64-tap composite tables, NBK = 2):
+    32 config-4 rooms = 1,024 channels (split) against 8-room batches
+    (combined sweep), and one room against the oracle."""
+    w = workloads.build(4, 32)
+    w.jobs["n_images"] = np.minimum(w.jobs["n_images"], 12000)  # no segmented channels
+    big = engine.simulate_jobs(w.sample_rate, w.jobs, w.mics, include_early=True)
+    pb = engine.prepare(w.sample_rate, w.jobs, w.mics)
+    db = engine.DeviceBatch(pb)
+    assert db.launch_count(True) == db.launch_count(False) + 1
+    nj = len(w.jobs)
+    for lo in range(0, nj, 16):  # 8 rooms x 2 sources x 16 mics = 256 channels: combined
+        jobs, mics = engine.split_jobs(w.jobs, w.mics, lo, min(nj, lo + 16))
+        part = engine.simulate_jobs(w.sample_rate, jobs, mics, include_early=True)
+        for j in range(len(jobs)):
+            assert torch.equal(big.job_view(lo + j), part.job_view(j))
+            assert torch.equal(big.job_view(lo + j, "early"), part.job_view(j, "early"))
+    J = w.jobs[3]
+    job = P.Job(room=tuple(float(x) for x in J["room"]), mics=w.mics[J["mic_off"]: J["mic_off"] + J["n_mics"]].copy(),
+                center=np.array(J["center"]), source=(float(J["d0"]), float(J["az"]), float(J["el"])),
+                t60=float(J["t60"]), sample_rate=w.sample_rate, num_images=int(J["n_images"]),
+                seed=int(J["seed"]), source_index=int(J["source_index"]))
+    full_o, early_o, _ = P.render(job, include_early=True)
+    assert rel_err(big.job_view(3).cpu().numpy(), full_o) <= TOL
+    assert rel_err(big.job_view(3, "early").cpu().numpy(), early_o) <= TOL
